@@ -1,0 +1,88 @@
+"""ctypes front of the seeded segment generator (include/synth.h, synth/synth_core.h).
+
+Input generator only — it holds none of the clipping arithmetic, so both the oracle
+tests and the CUDA path may use it.  The host and device twins are bit-identical.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SO = os.path.join(_HERE, "libsynth.so")
+_lib = None
+_lock = threading.Lock()
+
+UNIFORM, MIX, ADVERSARIAL = 0, 1, 2
+CAT_INSIDE, CAT_CROSSING, CAT_OUTSIDE = 0, 1, 2
+TAG_NEAR = 0x80
+
+# seed_C = 0x11105450 + config number
+SEED_BASE = 0x11105450
+
+
+def seed_for(config_no: int, extra: int = 0) -> int:
+    return SEED_BASE + config_no + (extra << 8)
+
+
+def mix_thresholds(p_in: float, p_cross: float):
+    """Probabilities -> the uint32 thresholds floor(p * 2^32) of the MIX family."""
+    return int(p_in * 2**32) & 0xFFFFFFFF, int(p_cross * 2**32) & 0xFFFFFFFF
+
+
+def plane_stride(n: int) -> int:
+    """ld for n segments: n rounded up to a multiple of 32 elements (>= 32)."""
+    return max(32, (n + 31) // 32 * 32)
+
+
+def lib():
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(_SO):
+                import build_all  # noqa: PLC0415
+                build_all.build_synth()
+            L = ctypes.CDLL(_SO)
+            P, I64, U64, U32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint32
+            for s in ("f32", "f64"):
+                f = getattr(L, "synth_fill_host_" + s)
+                f.argtypes = [ctypes.c_int, ctypes.c_int, U64, I64, I64, P, I64, P, U32, U32, ctypes.c_int]
+                f.restype = ctypes.c_int
+                f = getattr(L, "synth_fill_device_" + s)
+                f.argtypes = [ctypes.c_int, ctypes.c_int, U64, I64, I64, P, I64, P, U32, U32, P]
+                f.restype = ctypes.c_int
+            _lib = L
+    return _lib
+
+
+def fill_host(family, dim, seed, n, dtype=np.float32, i0=0, ld=None, p_in=0, p_cross=0, nthreads=None,
+              with_tag=True):
+    """Generate n segments (global indices i0..i0+n-1) on the host.
+    Returns (planes (2*dim, ld), tag uint8[n] or None)."""
+    dt = np.dtype(dtype)
+    ld = plane_stride(n) if ld is None else ld
+    planes = np.zeros((2 * dim, ld), dtype=dt)
+    tag = np.empty(max(n, 1), dtype=np.uint8) if with_tag else None
+    nthreads = nthreads or min(8, os.cpu_count() or 1)
+    f = lib().synth_fill_host_f32 if dt == np.float32 else lib().synth_fill_host_f64
+    st = f(family, dim, seed, i0, n, planes.ctypes.data, ld, tag.ctypes.data if tag is not None else None,
+           p_in, p_cross, nthreads)
+    if st != 0:
+        raise ValueError(f"synth_fill_host: status {st}")
+    return planes, (tag[:n] if tag is not None else None)
+
+
+def fill_device(planes_t, family, dim, seed, n, i0=0, p_in=0, p_cross=0, tag_t=None, stream=None):
+    """Generate into an existing CUDA tensor of shape (2*dim, ld) (torch), asynchronously."""
+    import torch  # noqa: PLC0415
+    ld = planes_t.shape[1]
+    f = lib().synth_fill_device_f32 if planes_t.dtype == torch.float32 else lib().synth_fill_device_f64
+    if stream is None:
+        stream = torch.cuda.current_stream().cuda_stream
+    st = f(family, dim, seed, i0, n, planes_t.data_ptr(), ld, tag_t.data_ptr() if tag_t is not None else None,
+           p_in, p_cross, stream)
+    if st != 0:
+        raise RuntimeError(f"synth_fill_device: status {st}")
