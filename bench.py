@@ -1,0 +1,379 @@
+"""bench.py — throughput of the B200 segment-clipping hot path (BASELINE.json metric:
+clipped segments/sec and achieved HBM GB/s, % of peak, at 1/2/4/8 B200).
+
+Workload (BASELINE.json configs[4], the metric's multi-GPU config):
+10^9 2D fp32 segments, endpoints on the 2^-22 grid uniform in [-1,2)^2, window [0,1]^2,
+one step = the whole hot path over the batch: the one-pass compacting clip (outcodes,
+trivial accept/reject, WEC intersection, clipped endpoints + flags, stable compaction +
+count) and, for N > 1, the NCCL allgather of the per-shard counts plus the offset kernel.
+Strong scaling: the 10^9 segments are split contiguously across the N ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the CPU oracle (oracle/) on the
+host cores over a bounded sample of the same workload (there is no reference code base:
+the paper is the reference).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_TOTAL = 10**9
+DIM = 2
+WORKLOAD = "C5: 2D fp32 compacting clip, 1e9 segments, endpoints uniform on the 2^-22 grid in [-1,2)^2, window [0,1]^2"
+METRIC = "clipped segments/sec"
+SEED = 0x11105450 + 5          # synth.seed_for(5)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=int(os.environ.get("WORLD_SIZE", "1")))
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=N_TOTAL, help="total segments (default 1e9)")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=40_000_000)
+    return ap.parse_args()
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.2)
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        rows = []
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                rows.append((float(f[0]), float(f[1]), f[4:8]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, r in rows for i, v in enumerate(r) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_oracle_rate(n_sample, nthreads):
+    """The oracle as it stands (oracle/libclip_oracle.so, plain scalar C) on host cores,
+    over the first n_sample segments of the workload; returns (seg/s, seconds, threads)."""
+    import numpy as np  # noqa: PLC0415
+    import oracle  # noqa: PLC0415  (cpu_baseline leg: the one place bench.py runs oracle/)
+    import synth  # noqa: PLC0415
+    planes, _ = synth.fill_host(synth.UNIFORM, DIM, SEED, n_sample, dtype=np.float32, with_tag=False)
+    ld = planes.shape[1]
+    out = np.empty_like(planes)
+    flags = np.empty(n_sample, dtype=np.uint8)
+    lo3 = np.zeros(3, np.float32)
+    hi3 = np.array([1, 1, 0], np.float32)
+    f = oracle.lib().oracle_clip_f32
+
+    def run(a, b):
+        f(DIM, lo3.ctypes.data, hi3.ctypes.data, planes.ctypes.data + 4 * a, ld, b - a, out.ctypes.data + 4 * a,
+          ld, flags.ctypes.data + a)
+
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=run, args=(n_sample * t // nthreads, n_sample * (t + 1) // nthreads))
+           for t in range(nthreads)]
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    dt = time.perf_counter() - t0
+    return n_sample / dt, dt, nthreads
+
+
+def host_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank, world):
+    """`--impl reference`: the oracle timed on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    nth = min(host_threads(), 64)
+    n_s = args.cpu_sample
+    cpu_oracle_rate(min(n_s, 1_000_000), nth)   # warm-up (page-in, thread start)
+    rates = []
+    total_t = 0.0
+    for _ in range(args.steps):
+        r, dt, _ = cpu_oracle_rate(n_s, nth)
+        rates.append(r)
+        total_t += dt
+        if total_t > 120:
+            break
+    v = statistics.median(rates)
+    sample = f"first {n_s} segments of the workload per step, {len(rates)} steps, {nth} threads (static split)"
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "segments/s", "n_gpus": world,
+            "steps": len(rates), "warmup": args.warmup, "ms_per_step": 1e3 * n_s / v, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "n_total": args.n, "sample": n_s, "parallelism": "host threads"},
+            "cpu_baseline": {"value": v, "unit": "segments/s", "cores": nth, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "segments/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch  # noqa: PLC0415
+    import torch.distributed as dist  # noqa: PLC0415
+    import synth  # noqa: PLC0415
+    from paper_1110_5450_b200 import clipseg  # noqa: PLC0415
+    from paper_1110_5450_b200.shard import shard_range  # noqa: PLC0415
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream()
+    start, stop = shard_range(args.n, world, rank)
+    n = stop - start
+
+    # inputs resident in HBM (generated on device by the seeded generator; not timed)
+    planes = clipseg.empty_planes(n, DIM, torch.float32, dev)
+    synth.fill_device(planes, synth.UNIFORM, DIM, SEED, n, i0=start)
+    bufs = clipseg.CompactBuffers(n, DIM, torch.float32, dev, with_index=False, with_flags=True)
+    counts = torch.zeros(world, dtype=torch.int64, device=dev)
+    offs = torch.zeros(2, dtype=torch.int64, device=dev)
+    w = clipseg.make_window([0.0, 0.0], [1.0, 1.0])
+    sp = stream.cuda_stream
+    launches_per_step = 1 + (1 if world > 1 else 0)
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        st = clipseg.clip_segments_compact_f32(planes.data_ptr(), planes.stride(0), n, ctypes.byref(w),
+                                               bufs.out.data_ptr(), bufs.out.stride(0), None, start,
+                                               bufs.flags.data_ptr(), bufs.count.data_ptr(), bufs.ws.data_ptr(),
+                                               bufs.ws.numel(), sp)
+        if ev is not None:
+            ev[1].record(stream)
+        if st != 0:
+            raise RuntimeError(clipseg.clip_status_string(st))
+        if world > 1:
+            dist.all_gather_into_tensor(counts, bufs.count)
+            clipseg.clip_shard_offsets(counts.data_ptr(), world, rank, offs.data_ptr(), offs.data_ptr() + 8, sp)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0.record(stream)
+        for k in range(args.steps):
+            step(kev[k])
+        t1.record(stream)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = t0.elapsed_time(t1)
+    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+    cnt = int(bufs.count.item())
+    if world > 1:
+        t = torch.tensor([ms, kern_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, kern_ms = float(t[0]), float(t[1])
+        total = torch.tensor([cnt], dtype=torch.int64, device=dev)
+        dist.all_reduce(total)
+        visible_total = int(total.item())
+    else:
+        visible_total = cnt
+    ms_per_step = ms / args.steps
+    value = args.n / (ms_per_step / 1e3)
+
+    # algorithmic bytes of the dominant kernel, per launch on this rank
+    alg_bytes = n * (2 * DIM * 4 + 1) + cnt * (2 * DIM * 4)
+    peak, peak_src = measured_peak()
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        if tj.get("n") == n:
+            traffic = tj.get("dram_bytes_per_launch")
+    except Exception:
+        pass
+
+    # sampled parity of this run's output against the oracle (outside the timed region)
+    parity = sampled_parity(torch, bufs, n, start, rank)
+
+    # end to end through the public host-buffer API (pinned host memory, H2D + D2H timed)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(torch, dist, clipseg, synth, args, world, rank, dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        nth = min(host_threads(), 64)
+        r, dt, nth = cpu_oracle_rate(args.cpu_sample, nth)
+        cpu = {"value": r, "unit": "segments/s", "cores": nth, "kind": "oracle",
+               "sample": f"first {args.cpu_sample} segments of the workload ({dt:.1f} s wall, {nth} threads)"}
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    line = {
+        "metric": METRIC, "value": value, "unit": "segments/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n_total": args.n, "n_per_gpu": n, "dim": DIM, "flags": True,
+                   "out_index": False, "visible_fraction": visible_total / args.n,
+                   "l2": f"no flush: inputs {16 * n / 1e9:.1f} GB per GPU >> 126 MB L2",
+                   "parallelism": f"shard{world} (contiguous; NCCL allgather of counts)"},
+        "hbm_gbs_step": alg_bytes / (ms_per_step / 1e3) / 1e9,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "clip_compact_kernel<float,2>", "kernel_ms": kern_ms,
+                     "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src},
+        "clocks": clk.summary(),
+        "gpu_launches": launches_per_step * args.steps,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "parity": parity,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def sampled_parity(torch, bufs, n, start, rank, m=2000):
+    import numpy as np  # noqa: PLC0415
+    import oracle  # noqa: PLC0415
+    import synth  # noqa: PLC0415
+    rng = np.random.default_rng(rank)
+    idx = np.unique(np.concatenate([rng.integers(0, n, m), [0, n - 1]]))
+    P = np.zeros((2 * DIM, synth.plane_stride(len(idx))), np.float32)
+    for j, i in enumerate(idx):
+        p, _ = synth.fill_host(synth.UNIFORM, DIM, SEED, 1, i0=start + int(i), nthreads=1, with_tag=False)
+        P[:, j] = p[:, 0]
+    want, wfl = oracle.clip(P, len(idx), [0, 0], [1, 1], DIM)
+    fl = bufs.flags[:n]
+    ti = torch.from_numpy(idx).to(fl.device)
+    ok = np.array_equal(fl[ti].cpu().numpy(), wfl)
+    pos = torch.cumsum(fl, 0, dtype=torch.int32) - 1
+    vis = np.nonzero(wfl)[0]
+    rows = pos[ti[torch.from_numpy(vis).to(fl.device)]].long()
+    got = bufs.out[:, rows].cpu().numpy()
+    ok = ok and np.array_equal(got.view(np.uint32), want[:, vis].view(np.uint32))
+    del pos
+    return f"{'ok' if ok else 'MISMATCH'}: {len(idx)} sampled segments bit-exact vs oracle"
+
+
+def run_e2e(torch, dist, clipseg, synth, args, world, rank, dev):
+    """Same metric through the public C-ABI host-buffer entry (clip_segments_compact_host_f32):
+    pinned host planes in, compacted planes + flags + count out; copies inside the timed region."""
+    import numpy as np  # noqa: PLC0415
+    from paper_1110_5450_b200.shard import shard_range  # noqa: PLC0415
+    start, stop = shard_range(args.n, world, rank)
+    n = stop - start
+    try:
+        h_in = torch.empty((2 * DIM, clipseg.clip_plane_stride(n)), dtype=torch.float32, pin_memory=True)
+        h_out = torch.empty_like(h_in, pin_memory=True)
+        h_flags = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    except Exception as e:  # host memory too small for the full workload
+        return {"value": None, "unit": "segments/s", "error": f"pinned alloc failed: {e}"[:200]}
+    d_tmp = clipseg.empty_planes(min(n, 1 << 26), DIM, torch.float32, dev)
+    for a in range(0, n, 1 << 26):   # fill host input from the device generator, chunk by chunk (not timed)
+        m = min(1 << 26, n - a)
+        synth.fill_device(d_tmp, synth.UNIFORM, DIM, SEED, m, i0=start + a)
+        h_in[:, a:a + m].copy_(d_tmp[:, :m])
+    del d_tmp
+    chunk = 1 << 25
+    staging = torch.empty(int(clipseg.clip_host_staging_bytes(DIM, 4, min(chunk, n))), dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+    cnt, staging = clipseg.clip_compact_host(h_in, n, [0, 0], [1, 1], h_out, h_flags=h_flags, chunk=chunk,
+                                             staging=staging)  # warm-up
+    times = []
+    for _ in range(max(args.e2e_steps, 1)):
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        cnt, _ = clipseg.clip_compact_host(h_in, n, [0, 0], [1, 1], h_out, h_flags=h_flags, chunk=chunk,
+                                           staging=staging)
+        torch.cuda.synchronize()
+        times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    if world > 1:
+        tt = torch.tensor([t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    return {"value": args.n / t, "unit": "segments/s", "h2d_bytes_per_step": 2 * DIM * 4 * n,
+            "d2h_bytes_per_step": 2 * DIM * 4 * cnt + n + 8, "api": "clip_segments_compact_host_f32",
+            "chunk": chunk, "s_per_step": t, "timer": "host wall clock around the blocking call, max over ranks"}
+
+
+if __name__ == "__main__":
+    main()

@@ -77,6 +77,16 @@ def build_clipseg(force=False, verbose=False):
     return CLIPSEG_SO
 
 
+def build_trace():
+    """Debug build of the library with per-tile timeline tracing (scripts/trace_compact.py)."""
+    srcs = _clipseg_sources()
+    out = os.path.join(ROOT, "build", "libclipseg_trace.so")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cus = [os.path.relpath(s, ROOT) for s in srcs if s.endswith(".cu")]
+    _run([NVCC, *ARCH, *NVCC_FP, *NVCC_COMMON, "-DCLIPSEG_TRACE", "-Iinclude", *cus, "-o", out])
+    return out
+
+
 def build(force=False, verbose=False):
     build_synth(force)
     build_oracle(force)

@@ -1,0 +1,120 @@
+/* include/clipseg.h — C ABI of the B200 segment-clipping library (libclipseg.so).
+ *
+ * The operation.  Batched clipping of line segments P0P1 against an axis-aligned,
+ * CLOSED window [lo, hi] (2D or 3D) by outcode ("region code") classification with
+ * trivial accept / trivial reject and the window-edge-coordinate (WEC) intersection
+ * alpha = WEC(P0) / (WEC(P0) - WEC(P1)), producing each segment's clipped endpoints
+ * and its visible flag, plus a stable compacting variant that returns only the visible
+ * segments and their count.  PAPER.md names the operation only through its macros
+ * \clip, \outcode, \wec, \WEC; its one clip is the closed
+ * interval [r_min, r_max] of §5.2, which fixes "closed".  The exact
+ * rule set (R1-R10: WEC, outcode bits, trivial cases, alpha per straddled edge,
+ * t_in/t_out, visibility, endpoint snap/fma/clamp, canonical NaN, non-finite inputs,
+ * stable compaction) is DESIGN.md §3 / SURVEY.md §8(c); results are bit-identical to
+ * the CPU oracle (oracle/clip_oracle.c) on every input.
+ *
+ * Layout.  Planar structure-of-arrays: 2*dim planes of `ld` elements, plane
+ * c = e*dim + k holds coordinate k of endpoint e, i.e. x0, y0, [z0], x1, y1, [z1];
+ * segment i's coordinate sits at ptr[c*ld + i].  Requirements (else CLIP_EALIGN):
+ * base pointers 16-byte aligned, ld*sizeof(element) a multiple of 16, ld >= n
+ * (all ld elements of every plane must be addressable: kernels may read, never
+ * write, the padding between n and ld); flags 4-byte aligned; out_index 8-byte aligned.
+ * clip_plane_stride(n) gives the canonical ld (n rounded up to 32 elements, >= 32).
+ *
+ * Memory and streams.  Every pointer is a DEVICE pointer unless its name starts with
+ * h_ or its comment says host; `win` is always a host pointer (copied into kernel
+ * parameters).  Calls are asynchronous on `stream` (a cudaStream_t; NULL = legacy
+ * default stream), except clip_segments_compact_host_* which returns when done.  The
+ * caller owns every buffer, including workspaces; the library never allocates or
+ * frees, keeps no state beyond cached device attributes, and is reentrant.
+ *
+ * Errors.  Functions return CLIP_OK (0) or a negative clip_status and never throw.
+ * n < 0, a required pointer NULL, dim not in {2,3}, a non-finite window or lo > hi
+ * -> CLIP_EINVAL (lo == hi is allowed: a degenerate window).  Misalignment ->
+ * CLIP_EALIGN.  Workspace/staging too small -> CLIP_ENOSPACE.  A CUDA launch or
+ * runtime error -> CLIP_ECUDA.  n == 0 is CLIP_OK with no kernel launch.
+ */
+#ifndef CLIPSEG_H_
+#define CLIPSEG_H_
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CLIP_OK = 0,
+  CLIP_EINVAL = -1,
+  CLIP_EALIGN = -2,
+  CLIP_ENOSPACE = -3,
+  CLIP_ECUDA = -4
+} clip_status;
+
+/* The clip window: lo[k] <= hi[k] for k < dim; entries k >= dim are ignored. */
+typedef struct { float lo[3], hi[3]; int dim; } clip_window_f32;
+typedef struct { double lo[3], hi[3]; int dim; } clip_window_f64;
+
+/* Canonical plane stride (elements) for n segments: n rounded up to a multiple of 32, >= 32. */
+int64_t clip_plane_stride(int64_t n);
+
+/* Human-readable name of a status code (static string). */
+const char* clip_status_string(int status);
+
+/* ---- Dense clip (rules R1-R9): every segment -> clipped endpoints + flag --------------
+ * in:    2*dim planes (ld_in), n segments.
+ * out:   2*dim planes (ld_out); row i = clipped Q0,Q1 of segment i if visible, else the
+ *        canonical quiet NaN (0x7FC00000 / 0x7FF8000000000000) in every plane.
+ *        out == in (same ld) is allowed: each thread reads its segments before writing.
+ * flags: n bytes (nullable): 1 visible, 0 invisible. */
+int clip_segments_f32(const float* in, int64_t ld_in, int64_t n, const clip_window_f32* win,
+                      float* out, int64_t ld_out, uint8_t* flags, void* stream);
+int clip_segments_f64(const double* in, int64_t ld_in, int64_t n, const clip_window_f64* win,
+                      double* out, int64_t ld_out, uint8_t* flags, void* stream);
+
+/* ---- Stable compacting clip (R1-R10), one pass with a decoupled look-back scan --------
+ * out:       2*dim planes (ld_out >= n): rows [0, count) hold the visible segments' clipped
+ *            endpoints in increasing input index; rows >= count are not written.
+ *            out must not overlap in.
+ * out_index: (nullable) int64[count]: index_base + input index of each kept segment.
+ * flags:     (nullable) n bytes, as in the dense call.
+ * d_count:   one int64 in device memory receiving count (the caller synchronises).
+ * workspace: device scratch of clip_compact_workspace_bytes(n) bytes (tile-claim counter
+ *            and per-tile look-back status words); reset by the call itself. */
+size_t clip_compact_workspace_bytes(int64_t n);
+int clip_segments_compact_f32(const float* in, int64_t ld_in, int64_t n, const clip_window_f32* win,
+                              float* out, int64_t ld_out, int64_t* out_index, int64_t index_base,
+                              uint8_t* flags, int64_t* d_count, void* workspace, size_t workspace_bytes,
+                              void* stream);
+int clip_segments_compact_f64(const double* in, int64_t ld_in, int64_t n, const clip_window_f64* win,
+                              double* out, int64_t ld_out, int64_t* out_index, int64_t index_base,
+                              uint8_t* flags, int64_t* d_count, void* workspace, size_t workspace_bytes,
+                              void* stream);
+
+/* ---- Sharded mode: global offsets from the per-shard visible counts ------------------
+ * d_counts: P int64 counts (the allgathered c_r, rank order).  Writes
+ * *d_offset = sum_{r' < rank} c_r' and *d_total = sum_r c_r (both device int64).
+ * P >= 1, 0 <= rank < P, else CLIP_EINVAL. */
+int clip_shard_offsets(const int64_t* d_counts, int P, int rank, int64_t* d_offset, int64_t* d_total,
+                       void* stream);
+
+/* ---- End-to-end compacting clip from/to HOST buffers (pipelined, blocking) ------------
+ * h_in:    host planes (ld_in) of n segments; pinned (page-locked) memory gives full PCIe
+ *          bandwidth, pageable memory works but serialises the copies.
+ * h_out:   host planes (ld_out >= n) receiving rows [0, count) as in the device call.
+ * h_flags: (nullable) n host bytes.  h_count: host int64 receiving count.
+ * The input is streamed through the device in chunks of `chunk` segments: the H2D copy of
+ * chunk j+1, the clip of chunk j and the D2H copy of chunk j-1 overlap on three streams.
+ * d_staging: device scratch of clip_host_staging_bytes(dim, elem_bytes, chunk) bytes.
+ * Returns when all results are in host memory (synchronises its own streams only). */
+size_t clip_host_staging_bytes(int dim, int elem_bytes, int64_t chunk);
+int clip_segments_compact_host_f32(const float* h_in, int64_t ld_in, int64_t n, const clip_window_f32* win,
+                                   float* h_out, int64_t ld_out, uint8_t* h_flags, int64_t* h_count,
+                                   int64_t chunk, void* d_staging, size_t staging_bytes);
+int clip_segments_compact_host_f64(const double* h_in, int64_t ld_in, int64_t n, const clip_window_f64* win,
+                                   double* h_out, int64_t ld_out, uint8_t* h_flags, int64_t* h_count,
+                                   int64_t chunk, void* d_staging, size_t staging_bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CLIPSEG_H_ */

@@ -1,0 +1,208 @@
+"""Thin Python binding of libclipseg.so (include/clipseg.h).
+
+Argument marshalling only: every step of the clipping path runs in the library's
+sm_100a kernels.  The low-level functions carry the C names and take raw pointers;
+the helpers at the bottom take torch tensors (PyTorch provides device memory, streams
+and process groups — nothing else).  There is no fallback: if the shared library is
+missing or fails to load, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libclipseg.so")
+
+CLIP_OK, CLIP_EINVAL, CLIP_EALIGN, CLIP_ENOSPACE, CLIP_ECUDA = 0, -1, -2, -3, -4
+
+
+class clip_window_f32(ctypes.Structure):  # noqa: N801  (C name)
+    _fields_ = [("lo", ctypes.c_float * 3), ("hi", ctypes.c_float * 3), ("dim", ctypes.c_int)]
+
+
+class clip_window_f64(ctypes.Structure):  # noqa: N801
+    _fields_ = [("lo", ctypes.c_double * 3), ("hi", ctypes.c_double * 3), ("dim", ctypes.c_int)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"libclipseg.so not built at {LIB_PATH}: run `python build_all.py` "
+                          "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    P, I64, U8P, SZ = ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t
+    L.clip_plane_stride.argtypes = [I64]
+    L.clip_plane_stride.restype = I64
+    L.clip_status_string.argtypes = [ctypes.c_int]
+    L.clip_status_string.restype = ctypes.c_char_p
+    for s, W in (("f32", clip_window_f32), ("f64", clip_window_f64)):
+        f = getattr(L, "clip_segments_" + s)
+        f.argtypes = [P, I64, I64, ctypes.POINTER(W), P, I64, U8P, P]
+        f.restype = ctypes.c_int
+        f = getattr(L, "clip_segments_compact_" + s)
+        f.argtypes = [P, I64, I64, ctypes.POINTER(W), P, I64, P, I64, U8P, P, P, SZ, P]
+        f.restype = ctypes.c_int
+        f = getattr(L, "clip_segments_compact_host_" + s)
+        f.argtypes = [P, I64, I64, ctypes.POINTER(W), P, I64, U8P, ctypes.POINTER(I64), I64, P, SZ]
+        f.restype = ctypes.c_int
+    L.clip_compact_workspace_bytes.argtypes = [I64]
+    L.clip_compact_workspace_bytes.restype = SZ
+    L.clip_host_staging_bytes.argtypes = [ctypes.c_int, ctypes.c_int, I64]
+    L.clip_host_staging_bytes.restype = SZ
+    L.clip_shard_offsets.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P, P]
+    L.clip_shard_offsets.restype = ctypes.c_int
+    return L
+
+
+_lib = _load()
+
+# ---- the C entry points, same names ------------------------------------------------------
+clip_plane_stride = _lib.clip_plane_stride
+clip_status_string = _lib.clip_status_string
+clip_segments_f32 = _lib.clip_segments_f32
+clip_segments_f64 = _lib.clip_segments_f64
+clip_compact_workspace_bytes = _lib.clip_compact_workspace_bytes
+clip_segments_compact_f32 = _lib.clip_segments_compact_f32
+clip_segments_compact_f64 = _lib.clip_segments_compact_f64
+clip_shard_offsets = _lib.clip_shard_offsets
+clip_host_staging_bytes = _lib.clip_host_staging_bytes
+clip_segments_compact_host_f32 = _lib.clip_segments_compact_host_f32
+clip_segments_compact_host_f64 = _lib.clip_segments_compact_host_f64
+
+EXPORTED = ["clip_plane_stride", "clip_status_string", "clip_segments_f32", "clip_segments_f64",
+            "clip_compact_workspace_bytes", "clip_segments_compact_f32", "clip_segments_compact_f64",
+            "clip_shard_offsets", "clip_host_staging_bytes", "clip_segments_compact_host_f32",
+            "clip_segments_compact_host_f64"]
+
+
+class ClipError(RuntimeError):
+    def __init__(self, status, what):
+        super().__init__(f"{what}: {clip_status_string(status).decode()} ({status})")
+        self.status = status
+
+
+def _check(status, what):
+    if status != CLIP_OK:
+        raise ClipError(status, what)
+
+
+def make_window(lo, hi, dtype="f32"):
+    dim = len(lo)
+    W = clip_window_f32 if dtype == "f32" else clip_window_f64
+    w = W()
+    for k in range(dim):
+        w.lo[k] = lo[k]
+        w.hi[k] = hi[k]
+    w.dim = dim
+    return w
+
+
+# ---- torch-level helpers (allocation + marshalling) --------------------------------------
+def _torch():
+    import torch  # noqa: PLC0415
+    return torch
+
+
+def _sfx(t):
+    torch = _torch()
+    if t.dtype == torch.float32:
+        return "f32"
+    if t.dtype == torch.float64:
+        return "f64"
+    raise TypeError(f"unsupported dtype {t.dtype}")
+
+
+def _stream(stream):
+    torch = _torch()
+    return (stream if stream is not None else torch.cuda.current_stream()).cuda_stream
+
+
+def empty_planes(n, dim, dtype, device="cuda"):
+    """A (2*dim, clip_plane_stride(n)) planar buffer."""
+    torch = _torch()
+    return torch.empty((2 * dim, clip_plane_stride(n)), dtype=dtype, device=device)
+
+
+def clip(planes, n, lo, hi, out=None, flags=None, want_flags=True, stream=None):
+    """Dense clip of n segments held in `planes` (2*dim, ld) -> (out, flags)."""
+    torch = _torch()
+    dim = planes.shape[0] // 2
+    sfx = _sfx(planes)
+    if out is None:
+        out = torch.empty_like(planes)
+    if flags is None and want_flags:
+        flags = torch.empty(max(n, 1), dtype=torch.uint8, device=planes.device)
+    w = make_window(lo, hi, sfx)
+    f = clip_segments_f32 if sfx == "f32" else clip_segments_f64
+    _check(f(planes.data_ptr(), planes.stride(0), n, ctypes.byref(w), out.data_ptr(), out.stride(0),
+             flags.data_ptr() if flags is not None else None, _stream(stream)), "clip_segments_" + sfx)
+    return out, flags
+
+
+class CompactBuffers:
+    """Reusable outputs + workspace for the compacting clip of up to n segments."""
+
+    def __init__(self, n, dim, dtype, device="cuda", with_index=False, with_flags=False):
+        torch = _torch()
+        self.n, self.dim = n, dim
+        self.out = empty_planes(n, dim, dtype, device)
+        self.count = torch.zeros(1, dtype=torch.int64, device=device)
+        self.ws = torch.empty(max(int(clip_compact_workspace_bytes(n)), 128), dtype=torch.uint8, device=device)
+        self.index = torch.empty(max(n, 1), dtype=torch.int64, device=device) if with_index else None
+        self.flags = torch.empty(max(n, 1), dtype=torch.uint8, device=device) if with_flags else None
+
+
+def clip_compact(planes, n, lo, hi, bufs: CompactBuffers | None = None, with_index=False, with_flags=False,
+                 index_base=0, stream=None):
+    """Stable compacting clip -> CompactBuffers (out rows [0, count) valid; count on device)."""
+    dim = planes.shape[0] // 2
+    sfx = _sfx(planes)
+    if bufs is None:
+        bufs = CompactBuffers(n, dim, planes.dtype, planes.device, with_index, with_flags)
+    w = make_window(lo, hi, sfx)
+    f = clip_segments_compact_f32 if sfx == "f32" else clip_segments_compact_f64
+    _check(f(planes.data_ptr(), planes.stride(0), n, ctypes.byref(w), bufs.out.data_ptr(), bufs.out.stride(0),
+             bufs.index.data_ptr() if bufs.index is not None else None, index_base,
+             bufs.flags.data_ptr() if bufs.flags is not None else None, bufs.count.data_ptr(),
+             bufs.ws.data_ptr(), bufs.ws.numel(), _stream(stream)), "clip_segments_compact_" + sfx)
+    return bufs
+
+
+def clip_compact_host(h_planes, n, lo, hi, h_out, h_flags=None, chunk=1 << 24, staging=None):
+    """End-to-end compacting clip of HOST planes (numpy or CPU torch, ideally pinned) through
+    the device; returns the visible count.  `staging` (a CUDA uint8 tensor) is reused if given."""
+    torch = _torch()
+    import numpy as np  # noqa: PLC0415
+
+    def ptr_ld(a):
+        if isinstance(a, np.ndarray):
+            return a.ctypes.data, a.strides[0] // a.itemsize, a.dtype
+        return a.data_ptr(), a.stride(0), a.dtype
+
+    pin, ld_in, dt = ptr_ld(h_planes)
+    pout, ld_out, _ = ptr_ld(h_out)
+    dim = h_planes.shape[0] // 2
+    f64 = dt in (np.float64, torch.float64)
+    esz = 8 if f64 else 4
+    chunk = max(1, min(chunk, n)) if n > 0 else 1
+    need = int(clip_host_staging_bytes(dim, esz, chunk))
+    if staging is None or staging.numel() < need:
+        staging = torch.empty(need, dtype=torch.uint8, device="cuda")
+    w = make_window(lo, hi, "f64" if f64 else "f32")
+    cnt = ctypes.c_int64(0)
+    fl = None
+    if h_flags is not None:
+        fl = h_flags.ctypes.data if isinstance(h_flags, np.ndarray) else h_flags.data_ptr()
+    f = clip_segments_compact_host_f64 if f64 else clip_segments_compact_host_f32
+    _check(f(pin, ld_in, n, ctypes.byref(w), pout, ld_out, fl, ctypes.byref(cnt), chunk, staging.data_ptr(),
+             staging.numel()), "clip_segments_compact_host")
+    return cnt.value, staging
+
+
+def shard_offsets(counts_t, rank, stream=None):
+    """Exclusive prefix (offset of `rank`) and total of allgathered int64 counts (device)."""
+    torch = _torch()
+    off = torch.empty(2, dtype=torch.int64, device=counts_t.device)
+    _check(clip_shard_offsets(counts_t.data_ptr(), counts_t.numel(), rank, off.data_ptr(), off.data_ptr() + 8,
+                              _stream(stream)), "clip_shard_offsets")
+    return off

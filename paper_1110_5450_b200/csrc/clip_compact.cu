@@ -1,0 +1,489 @@
+// clip_compact.cu — K3: stable compacting clip in one pass (R1-R10).
+//
+// Single-pass stream compaction with tile aggregates published in global memory
+// (decoupled look-back, Merrill & Garland), organised for sm_100a as a warp-specialised,
+// software-pipelined persistent kernel.  Co-resident grid (cooperative launch):
+//
+//  * block 0 is the GLOBAL SCANNER: one warp walks the per-tile status words in tile order,
+//    512 per probe, and turns every run of published aggregates (flag A) into inclusive
+//    prefixes (flag P).  A tile's offset is thus known about one L2 round trip after the
+//    last of its predecessors has published, with no redundant per-tile walks;
+//
+//  * every other block claims block tiles of BT = NSUB x 128 segments in increasing order
+//    from an atomic counter (the first of its compute warps to become free claims, so claim
+//    order follows the order blocks start computing) and runs
+//      - 8 compute warps.  Per sub-tile (32 lanes x 4 segments, one 128-bit load per plane
+//        per lane, the next sub-tile's loads in flight while this one is clipped) a warp
+//        classifies and clips its segments (clip_math.cuh), stores the flags, warp-scans the
+//        visible counts and stages the visible rows, compacted, in its slot of stage buffer
+//        k % NBUF.  The last warp to finish a tile publishes its aggregate (flag A).  Then
+//        each warp copies ITS OWN staged rows of tile k - (NBUF-1), whose offset is known by
+//        then, to their global rows (coalesced) — so compute warps neither wait for one
+//        another nor, normally, for the offsets;
+//      - 1 scan warp: once tile k's counts are in, it prefix-sums the NSUB sub-tile counts,
+//        waits for the scanner's inclusive prefix of the tile and hands the offsets over.
+//
+// Hand-offs inside a block use shared-memory mbarriers (compute warps -> scan warp: 8
+// arrivals per tile; scan warp -> compute warps: 1; claiming warp -> all: the tile id, a
+// ring of 4).  Status words are 64-bit: flag in bits 62-63 (0 not ready, 1 aggregate,
+// 2 inclusive prefix), value in bits 0-61.  The scanner writes the total count.
+#include "clip_kernels.cuh"
+#include "vec_io.cuh"
+
+namespace clipseg {
+
+#ifdef CLIPSEG_TRACE
+// Debug build only (scripts/trace_compact.py): per-tile timeline in %globaltimer ns.
+// slots: 0 claimed, 1 compute start, 2 aggregate published, 3 prefix wait start,
+// 4 prefix seen by the block, 5 prefix published by the scanner, 6 copy start, 7 block id.
+constexpr int kTraceTiles = 1 << 19;
+__device__ unsigned long long g_trace[kTraceTiles * 8];
+__device__ __forceinline__ unsigned long long trace_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define CLIP_TRACE(tile, slot, val)                                                \
+  do {                                                                              \
+    if ((tile) >= 0 && (tile) < kTraceTiles) g_trace[(tile) * 8 + (slot)] = (val); \
+  } while (0)
+#else
+#define CLIP_TRACE(tile, slot, val) \
+  do {                              \
+  } while (0)
+#endif
+
+namespace {
+
+constexpr unsigned long long kFlagA = 1ull << 62;
+constexpr unsigned long long kFlagP = 2ull << 62;
+constexpr unsigned long long kValueMask = (1ull << 62) - 1;
+constexpr int kComputeWarps = 8;
+constexpr int kThreads = (kComputeWarps + 1) * 32;  // + the scan warp
+constexpr int kScanPerLane = 16;                     // scanner: 512 tiles per probe
+
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+// release: the arriving thread's prior shared-memory writes are visible to the waiters
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_addr(bar))
+               : "memory");
+}
+// acquire: wait until the phase with the given parity has completed.  The suspend-time
+// hint lets the hardware park the warp until the phase flips instead of spinning, so
+// waiting warps leave the issue slots to the compute warps.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+
+// Block 0's scan warp: walks the tile statuses in order and turns every run of published
+// aggregates that follows the scanned prefix into inclusive prefixes.
+__device__ __noinline__ void global_scanner(unsigned long long* status, int64_t ntiles, int lane, int64_t* d_count) {
+  constexpr int M = kScanPerLane;
+  int64_t base = 0;
+  unsigned long long running = 0;
+  unsigned backoff = 32;
+  while (base < ntiles) {
+    unsigned long long s[M];
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      const int64_t idx = base + lane * M + j;
+      s[j] = (idx < ntiles) ? ld_relaxed(status + idx) : 0ull;  // past the end: never ready
+    }
+    int myx = M;  // this lane's first not-ready tile
+#pragma unroll
+    for (int j = M - 1; j >= 0; --j)
+      if ((s[j] >> 62) == 0u) myx = j;
+    const unsigned xmask = __ballot_sync(0xFFFFFFFFu, myx < M);
+    const int fl = xmask ? __ffs(xmask) - 1 : 32;
+    const int ready = (fl == 32) ? 32 * M : fl * M + __shfl_sync(0xFFFFFFFFu, myx, fl & 31);
+    if (ready == 0) {
+      __nanosleep(backoff);
+      backoff = backoff < 256 ? 2 * backoff : 256;
+      continue;
+    }
+    backoff = 32;
+    unsigned long long vsum = 0;
+#pragma unroll
+    for (int j = 0; j < M; ++j)
+      if (lane * M + j < ready) vsum += s[j] & kValueMask;
+    unsigned long long incl = vsum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    unsigned long long run = running + incl - vsum;
+#pragma unroll
+    for (int j = 0; j < M; ++j) {
+      if (lane * M + j < ready) {
+        run += s[j] & kValueMask;
+        st_relaxed(status + base + lane * M + j, kFlagP | run);
+        CLIP_TRACE(base + lane * M + j, 5, trace_now());
+      }
+    }
+    running += __shfl_sync(0xFFFFFFFFu, incl, 31);
+    base += ready;
+  }
+  if (lane == 0) *d_count = (int64_t)running;
+}
+
+}  // namespace
+
+template <typename T, int D> struct CompactShape {
+  static constexpr int V = Vec16<T>::N;                 // segments per 128-bit vector
+  static constexpr int IT = compact_items<T>();          // vectors per lane per sub-tile
+  static constexpr int SUB = 32 * V * IT;                // 128 segments per sub-tile
+  static constexpr int NSUB = compact_subtiles<T, D>();  // sub-tiles per block tile
+  static constexpr int BT = NSUB * SUB;
+  static constexpr int NBUF = compact_buffers<T, D>();   // staged tiles in flight per block
+  static constexpr int SLOT = 2 * D * SUB;               // staged elements per sub-tile
+  static constexpr size_t kStageBytes = (size_t)NBUF * NSUB * SLOT * sizeof(T);
+  static constexpr size_t kSmemBytes = kStageBytes + (size_t)NBUF * NSUB * SUB;  // + local indices
+  static constexpr int kMinBlocks = (sizeof(T) == 4 && D == 2) ? 2 : 1;
+};
+
+template <typename T, int D>
+__global__ void __launch_bounds__(kThreads, CompactShape<T, D>::kMinBlocks) clip_compact_kernel(
+    const T* __restrict__ in, int64_t ld_in, int64_t n, Window<T, D> w, T* __restrict__ out, int64_t ld_out,
+    int64_t* __restrict__ out_index, int64_t index_base, uint8_t* __restrict__ flags, int64_t* __restrict__ d_count,
+    unsigned long long* __restrict__ ws, int64_t ntiles) {
+  typedef CompactShape<T, D> S;
+  constexpr int V = S::V, IT = S::IT, SUB = S::SUB, NSUB = S::NSUB, BT = S::BT, SLOT = S::SLOT, NBUF = S::NBUF;
+  constexpr int PER_WARP = NSUB / kComputeWarps;
+  static_assert(NSUB % kComputeWarps == 0 && NSUB <= 32 && NBUF >= 2 && NBUF <= 4, "tile layout");
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* stage = reinterpret_cast<T*>(smem_raw);            // [NBUF][NSUB][2D][SUB]
+  uint8_t* lidx = smem_raw + S::kStageBytes;            // [NBUF][NSUB][SUB]
+  __shared__ int s_cnt[NBUF][NSUB], s_pre[NBUF][NSUB];
+  __shared__ int64_t s_prefix[NBUF];
+  __shared__ int s_done[NBUF];                           // compute warps finished with buffer b
+  __shared__ int64_t s_tile[4];                          // tile of iteration k in slot k & 3
+  __shared__ int s_claim[4];                             // compute warps that reached slot k & 3
+  __shared__ __align__(8) uint64_t mb_cnt[NBUF];         // compute warps -> scan warp
+  __shared__ __align__(8) uint64_t mb_pre[NBUF];         // scan warp -> compute warps
+  __shared__ __align__(8) uint64_t mb_tile[4];           // claiming warp -> all
+
+  unsigned long long* counter = ws;
+  unsigned long long* status = ws + kWsHeaderBytes / 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < NBUF; ++q) {
+      s_done[q] = 0;
+      mbar_init(&mb_cnt[q], kComputeWarps);
+      mbar_init(&mb_pre[q], 1);
+    }
+    for (int q = 0; q < 4; ++q) {
+      s_claim[q] = 0;
+      mbar_init(&mb_tile[q], 1);
+    }
+    if (blockIdx.x != 0) {
+      s_tile[0] = (int64_t)atomicAdd(counter, 1ull);
+      mbar_arrive(&mb_tile[0]);
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) {  // block 0 only scans; it processes no tiles
+    if (warp == kComputeWarps) global_scanner(status, ntiles, lane, d_count);
+    return;
+  }
+
+  if (warp == kComputeWarps) {
+    // ------------------------------------------------------------------ scan warp
+    int b = 0;
+    unsigned par = 0;  // bit q: parity of the next phase of mb_cnt[q] / mb_pre[q]
+    for (int64_t k = 0;; ++k) {
+      mbar_wait(&mb_tile[k & 3], (uint32_t)((k >> 2) & 1));
+      const int64_t tile = s_tile[k & 3];
+      if (tile >= ntiles) break;
+      mbar_wait(&mb_cnt[b], (par >> b) & 1u);  // the compute warps' counts of tile k
+      const int c = (lane < NSUB) ? s_cnt[b][lane] : 0;
+      int incl = c;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+        if (lane >= d) incl += y;
+      }
+      if (lane < NSUB) s_pre[b][lane] = incl - c;
+      const int64_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      if (lane == 0) {
+        CLIP_TRACE(tile, 3, trace_now());
+        unsigned long long st;
+        while (((st = ld_relaxed(status + tile)) >> 62) != 2u)  // the scanner's inclusive prefix
+          __nanosleep(1000);  // it typically lands a few microseconds after the aggregate
+        CLIP_TRACE(tile, 4, trace_now());
+        CLIP_TRACE(tile, 7, blockIdx.x);
+        s_prefix[b] = (int64_t)(st & kValueMask) - total;
+        s_done[b] = 0;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&mb_pre[b]);  // tile k's offsets published
+      par ^= 1u << b;
+      b = (b + 1 == NBUF) ? 0 : b + 1;
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------------- compute warps
+  // Copies lag NBUF-1 tiles behind the compute: pend[q] is the tile of iteration k-1-q.
+  int64_t pend[NBUF - 1];
+  int pbuf[NBUF - 1];
+  unsigned ppar[NBUF - 1];
+#pragma unroll
+  for (int q = 0; q < NBUF - 1; ++q) {
+    pend[q] = ntiles;
+    pbuf[q] = 0;
+    ppar[q] = 0;
+  }
+  int b = 0;
+  unsigned par = 0;
+  bool claiming = true;
+  for (int64_t k = 0;; ++k) {
+    int64_t tile = ntiles;
+    if (claiming) {
+      if (k > 0 && lane == 0) {
+        // the first compute warp to reach tile k claims it
+        const int order = atomicAdd(&s_claim[k & 3], 1);
+        if (order == 0) {
+          s_tile[k & 3] = (int64_t)atomicAdd(counter, 1ull);
+          CLIP_TRACE(s_tile[k & 3], 0, trace_now());
+          mbar_arrive(&mb_tile[k & 3]);
+        } else if (order == kComputeWarps - 1) {
+          s_claim[k & 3] = 0;  // every warp has passed this slot; reused at iteration k + 4
+        }
+      }
+      mbar_wait(&mb_tile[k & 3], (uint32_t)((k >> 2) & 1));
+      tile = s_tile[k & 3];
+      if (tile >= ntiles) claiming = false;
+    }
+    if (tile < ntiles) {
+      if (warp == 0 && lane == 0) CLIP_TRACE(tile, 1, trace_now());
+      T* stg = stage + (size_t)b * NSUB * SLOT;
+      uint8_t* lix = lidx + (size_t)b * NSUB * SUB;
+      // segments of sub-tile `sub` still in range (SUB for every full sub-tile)
+      auto remaining = [&](int sub) -> int {
+        const int64_t r = n - (tile * BT + (int64_t)sub * SUB);
+        return r >= SUB ? SUB : (r > 0 ? (int)r : 0);
+      };
+      auto load = [&](int sub, T (&dst)[IT][2 * D][V]) {
+        const T* src = in + tile * BT + (int64_t)sub * SUB;
+        const int rem = remaining(sub);
+#pragma unroll
+        for (int j = 0; j < IT; ++j) {
+          const int o = (32 * j + lane) * V;
+          if (o < rem) {
+#pragma unroll
+            for (int c = 0; c < 2 * D; ++c) load_vec<T>(src + c * ld_in + o, dst[j][c]);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 2 * D; ++c)
+#pragma unroll
+              for (int v = 0; v < V; ++v) dst[j][c][v] = T(0);
+          }
+        }
+      };
+      T buf[2][IT][2 * D][V];
+      load(warp, buf[0]);  // sub-tile loads run one ahead of the clipping
+#pragma unroll
+      for (int r = 0; r < PER_WARP; ++r) {
+        const int sub = r * kComputeWarps + warp;
+        if (r + 1 < PER_WARP) load(sub + kComputeWarps, buf[(r + 1) & 1]);
+        const T (&plane)[IT][2 * D][V] = buf[r & 1];
+        const int rem = remaining(sub);
+        uint8_t* fl = flags ? flags + tile * BT + (int64_t)sub * SUB : nullptr;
+        T res[IT][2 * D][V];
+        unsigned vis[IT];
+#pragma unroll
+        for (int j = 0; j < IT; ++j) {
+          const int o = (32 * j + lane) * V;
+          const unsigned live = (o >= rem) ? 0u : (o + V <= rem ? (1u << V) - 1u : (1u << (rem - o)) - 1u);
+          vis[j] = clip_group<T, D, V, false>(plane[j], w, res[j]) & live;
+          if (fl) {
+            uint32_t packed = 0;
+#pragma unroll
+            for (int v = 0; v < V; ++v) packed |= ((vis[j] >> v) & 1u) << (8 * v);
+            if (o + V <= rem) {
+              if (V == 4) *reinterpret_cast<uint32_t*>(fl + o) = packed;
+              else *reinterpret_cast<uint16_t*>(fl + o) = (uint16_t)packed;
+            } else {
+              for (int v = 0; v < V; ++v)
+                if (o + v < rem) fl[o + v] = (uint8_t)((vis[j] >> v) & 1u);
+            }
+          }
+        }
+        // warp scan of the visible counts (item j in bit field 8 j)
+        unsigned cnt = 0;
+#pragma unroll
+        for (int j = 0; j < IT; ++j) cnt |= (unsigned)__popc(vis[j]) << (8 * j);
+        unsigned incl = cnt;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+          if (lane >= d) incl += y;
+        }
+        const unsigned tot_f = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        const unsigned excl_f = incl - cnt;
+        // stage the visible rows, compacted, at the front of this sub-tile's slot
+        T* st = stg + sub * SLOT;
+        int before = 0;
+#pragma unroll
+        for (int j = 0; j < IT; ++j) {
+          int pos = before + (int)((excl_f >> (8 * j)) & 0xFFu);
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            const bool on = (vis[j] >> v) & 1u;
+            if (on) {
+#pragma unroll
+              for (int c = 0; c < 2 * D; ++c) st[c * SUB + pos] = res[j][c][v];
+              if (out_index) lix[sub * SUB + pos] = (uint8_t)((32 * j + lane) * V + v);
+            }
+            pos += on;
+          }
+          before += (int)((tot_f >> (8 * j)) & 0xFFu);
+        }
+        if (lane == 0) s_cnt[b][sub] = before;
+      }
+      // the last compute warp to finish publishes the tile aggregate (flag A) at once
+      __syncwarp();
+      int last = 0;
+      if (lane == 0) {
+        __threadfence_block();
+        last = atomicAdd(&s_done[b], 1) == kComputeWarps - 1;
+      }
+      last = __shfl_sync(0xFFFFFFFFu, last, 0);
+      if (last) {
+        __threadfence_block();
+        int c = (lane < NSUB) ? ((volatile int*)s_cnt[b])[lane] : 0;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, d);
+        if (lane == 0) {
+          st_relaxed(status + tile, kFlagA | (unsigned long long)c);
+          CLIP_TRACE(tile, 2, trace_now());
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&mb_cnt[b]);  // counts of tile k published to the scan warp
+    }
+    // copy the rows of the oldest pending tile (iteration k - (NBUF-1)), then shift
+    constexpr int Q = NBUF - 2;
+    if (pend[Q] < ntiles) {
+      const int pb = pbuf[Q];
+      mbar_wait(&mb_pre[pb], ppar[Q]);  // its offsets are published
+      if (warp == 0 && lane == 0) CLIP_TRACE(pend[Q], 6, trace_now());
+      const int64_t prefix = s_prefix[pb];
+      const T* stg = stage + (size_t)pb * NSUB * SLOT;
+      const uint8_t* lix = lidx + (size_t)pb * NSUB * SUB;
+#pragma unroll
+      for (int r = 0; r < PER_WARP; ++r) {
+        const int sub = r * kComputeWarps + warp;  // the sub-tiles this warp staged
+        const int cnt = s_cnt[pb][sub];
+        const int64_t g0 = prefix + s_pre[pb][sub];
+        const T* st = stg + sub * SLOT;
+#pragma unroll
+        for (int c = 0; c < 2 * D; ++c) {
+          T* dst = out + c * ld_out + g0;
+#pragma unroll
+          for (int q = 0; q < SUB / 32; ++q) {
+            const int e = q * 32 + lane;
+            if (e < cnt) __stcs(dst + e, st[c * SUB + e]);
+          }
+        }
+        if (out_index) {
+          const int64_t ib = index_base + pend[Q] * BT + (int64_t)sub * SUB;
+#pragma unroll
+          for (int q = 0; q < SUB / 32; ++q) {
+            const int e = q * 32 + lane;
+            if (e < cnt) out_index[g0 + e] = ib + lix[sub * SUB + e];
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int q = Q; q > 0; --q) {
+      pend[q] = pend[q - 1];
+      pbuf[q] = pbuf[q - 1];
+      ppar[q] = ppar[q - 1];
+    }
+    pend[0] = tile;
+    pbuf[0] = b;
+    ppar[0] = (par >> b) & 1u;
+    if (tile < ntiles) par ^= 1u << b;
+    b = (b + 1 == NBUF) ? 0 : b + 1;
+    if (!claiming) {
+      bool any = false;
+#pragma unroll
+      for (int q = 0; q <= Q; ++q) any |= pend[q] < ntiles;
+      if (!any) break;
+    }
+  }
+}
+
+template <typename T, int D>
+cudaError_t launch_compact(const T* in, int64_t ld_in, int64_t n, const Window<T, D>& w, T* out, int64_t ld_out,
+                           int64_t* out_index, int64_t index_base, uint8_t* flags, int64_t* d_count, void* ws,
+                           cudaStream_t s) {
+  typedef CompactShape<T, D> S;
+  const int64_t ntiles = (n + S::BT - 1) / S::BT;
+  const size_t smem = S::kSmemBytes;
+  static int blocks_per_sm = 0;  // cached device attribute
+  if (!blocks_per_sm) {
+    cudaFuncSetAttribute(clip_compact_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, clip_compact_kernel<T, D>,
+                                                                  kThreads, smem);
+    if (e != cudaSuccess || blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  cudaError_t e = cudaMemsetAsync(ws, 0, kWsHeaderBytes + (size_t)ntiles * 8, s);
+  if (e != cudaSuccess) return e;
+  // block 0 is the global scanner; the cooperative launch keeps every block resident, so
+  // the scanner runs alongside the tiles it waits on
+  const int64_t cap = (int64_t)device_sm_count() * blocks_per_sm;
+  const int grid = (int)(ntiles + 1 < cap ? ntiles + 1 : cap);
+  unsigned long long* wsp = reinterpret_cast<unsigned long long*>(ws);
+  void* args[] = {(void*)&in,     (void*)&ld_in,     (void*)&n,          (void*)&w,     (void*)&out,
+                  (void*)&ld_out, (void*)&out_index, (void*)&index_base, (void*)&flags, (void*)&d_count,
+                  (void*)&wsp,    (void*)&ntiles};
+  return cudaLaunchCooperativeKernel((const void*)clip_compact_kernel<T, D>, dim3(grid), dim3(kThreads), args, smem,
+                                     s);
+}
+
+#ifdef CLIPSEG_TRACE
+extern "C" int clip_trace_read(void* host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, g_trace, bytes) == cudaSuccess ? 0 : -4;
+}
+extern "C" int clip_trace_clear() {
+  static unsigned long long* p = nullptr;
+  if (cudaGetSymbolAddress((void**)&p, g_trace) != cudaSuccess) return -4;
+  return cudaMemset(p, 0, sizeof(unsigned long long) * kTraceTiles * 8) == cudaSuccess ? 0 : -4;
+}
+#endif
+
+#define INST(T, D)                                                                                              \
+  template cudaError_t launch_compact<T, D>(const T*, int64_t, int64_t, const Window<T, D>&, T*, int64_t,      \
+                                            int64_t*, int64_t, uint8_t*, int64_t*, void*, cudaStream_t);
+INST(float, 2)
+INST(float, 3)
+INST(double, 2)
+INST(double, 3)
+#undef INST
+
+}  // namespace clipseg

@@ -1,0 +1,86 @@
+// clip_dense.cu — K2: the dense clip (every segment -> clipped endpoints + flag).
+//
+// One thread owns V consecutive segments (V = 4 fp32 / 2 fp64): one 128-bit load per
+// plane, the branch-free per-segment rules of clip_math.cuh, one 128-bit store per plane
+// and one packed flag store.  Grid-stride over a persistent grid sized to the device's
+// resident capacity (148 SMs x blocks/SM).  HBM-bound: 2*(2D*sizeof(T)) + 1 bytes moved
+// per segment.
+#include "clip_kernels.cuh"
+#include "vec_io.cuh"
+
+namespace clipseg {
+
+template <typename T, int D>
+__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 3 : 2) clip_dense_kernel(const T* in, int64_t ld_in, int64_t n, Window<T, D> w,
+                                                         T* out, int64_t ld_out, uint8_t* flags) {
+  constexpr int V = Vec16<T>::N;
+  const int64_t ngroups = (n + V - 1) / V;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  T nxt[2 * D][V];
+  if (g < ngroups) {
+#pragma unroll
+    for (int c = 0; c < 2 * D; ++c) load_vec<T>(in + c * ld_in + g * V, nxt[c]);
+  }
+  for (; g < ngroups; g += stride) {
+    const int64_t i = g * V;
+    T plane[2 * D][V];
+#pragma unroll
+    for (int c = 0; c < 2 * D; ++c)
+#pragma unroll
+      for (int v = 0; v < V; ++v) plane[c][v] = nxt[c][v];
+    if (g + stride < ngroups) {  // next group's loads in flight while this one is clipped
+#pragma unroll
+      for (int c = 0; c < 2 * D; ++c) load_vec<T>(in + c * ld_in + (g + stride) * V, nxt[c]);
+    }
+    T res[2 * D][V];
+    const unsigned bits = clip_group<T, D, V, true>(plane, w, res);
+    uint32_t vis = 0;  // one flag byte per segment
+#pragma unroll
+    for (int v = 0; v < V; ++v) vis |= ((bits >> v) & 1u) << (8 * v);
+    if (i + V <= n) {
+#pragma unroll
+      for (int c = 0; c < 2 * D; ++c) store_vec<T>(out + c * ld_out + i, res[c]);
+      if (flags) {
+        if (V == 4) *reinterpret_cast<uint32_t*>(flags + i) = vis;
+        else *reinterpret_cast<uint16_t*>(flags + i) = (uint16_t)vis;
+      }
+    } else {  // ragged tail: only rows < n are written
+      for (int v = 0; v < V; ++v) {
+        if (i + v < n) {
+#pragma unroll
+          for (int c = 0; c < 2 * D; ++c) out[c * ld_out + i + v] = res[c][v];
+          if (flags) flags[i + v] = (uint8_t)((vis >> (8 * v)) & 1u);
+        }
+      }
+    }
+  }
+}
+
+template <typename T, int D>
+cudaError_t launch_dense(const T* in, int64_t ld_in, int64_t n, const Window<T, D>& w, T* out, int64_t ld_out,
+                         uint8_t* flags, cudaStream_t s) {
+  constexpr int V = Vec16<T>::N, NT = 256;
+  static int blocks_per_sm = 0;  // cached device attribute
+  if (!blocks_per_sm) {
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, clip_dense_kernel<T, D>, NT, 0);
+    if (e != cudaSuccess || blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  const int64_t ngroups = (n + V - 1) / V;
+  const int64_t want = (ngroups + NT - 1) / NT;
+  const int64_t cap = (int64_t)device_sm_count() * blocks_per_sm;
+  const int grid = (int)(want < cap ? want : cap);
+  clip_dense_kernel<T, D><<<grid, NT, 0, s>>>(in, ld_in, n, w, out, ld_out, flags);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_dense<float, 2>(const float*, int64_t, int64_t, const Window<float, 2>&, float*,
+                                            int64_t, uint8_t*, cudaStream_t);
+template cudaError_t launch_dense<float, 3>(const float*, int64_t, int64_t, const Window<float, 3>&, float*,
+                                            int64_t, uint8_t*, cudaStream_t);
+template cudaError_t launch_dense<double, 2>(const double*, int64_t, int64_t, const Window<double, 2>&, double*,
+                                             int64_t, uint8_t*, cudaStream_t);
+template cudaError_t launch_dense<double, 3>(const double*, int64_t, int64_t, const Window<double, 3>&, double*,
+                                             int64_t, uint8_t*, cudaStream_t);
+
+}  // namespace clipseg

@@ -1,0 +1,46 @@
+// clip_kernels.cuh — internal launcher interface between the C ABI (clip_api.cu) and
+// the sm_100a kernels (clip_dense.cu, clip_compact.cu, clip_shard.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "clip_math.cuh"
+
+namespace clipseg {
+
+// Workspace of the compacting kernel: a 128-byte header (tile-claim counter) followed by
+// one 64-bit look-back status word per tile.
+constexpr int kCompactThreads = 256;
+constexpr size_t kWsHeaderBytes = 128;
+
+template <typename T> __host__ __device__ constexpr int vec_elems() { return 16 / (int)sizeof(T); }
+// Compacting kernel: a warp sub-tile is 32 lanes x 4 segments (fp64 lanes load two
+// 128-bit vectors); a block tile is compact_subtiles() sub-tiles; compact_buffers() block
+// tiles are staged in shared memory at once (the copy-out lags the compute by that many
+// minus one), sized to stay near 100 KB of shared memory per block.
+template <typename T> __host__ __device__ constexpr int compact_items() { return 4 / vec_elems<T>(); }
+template <typename T, int D> __host__ __device__ constexpr int compact_subtiles() {
+  return (sizeof(T) == 4 && D == 2) ? 16 : 8;
+}
+template <typename T, int D> __host__ __device__ constexpr int compact_buffers() {
+  return (sizeof(T) == 8 && D == 3) ? 2 : 3;
+}
+// Smallest block tile over all (T, D): the workspace is sized with it.
+constexpr int64_t kMinCompactTile = 8 * 128;
+
+template <typename T, int D>
+cudaError_t launch_dense(const T* in, int64_t ld_in, int64_t n, const Window<T, D>& w, T* out, int64_t ld_out,
+                         uint8_t* flags, cudaStream_t s);
+
+template <typename T, int D>
+cudaError_t launch_compact(const T* in, int64_t ld_in, int64_t n, const Window<T, D>& w, T* out, int64_t ld_out,
+                           int64_t* out_index, int64_t index_base, uint8_t* flags, int64_t* d_count, void* ws,
+                           cudaStream_t s);
+
+cudaError_t launch_shard_offsets(const int64_t* d_counts, int P, int rank, int64_t* d_offset, int64_t* d_total,
+                                 cudaStream_t s);
+
+// Number of SMs of the current device (cached per device).
+int device_sm_count();
+
+}  // namespace clipseg

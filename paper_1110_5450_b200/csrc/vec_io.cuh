@@ -1,0 +1,32 @@
+// vec_io.cuh — 128-bit streaming global loads/stores for the planar segment layout.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace clipseg {
+
+template <typename T> struct Vec16;
+template <> struct Vec16<float> {
+  typedef float4 type;
+  static constexpr int N = 4;
+  static __device__ __forceinline__ void unpack(const float4& v, float (&a)[4]) { a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w; }
+  static __device__ __forceinline__ float4 pack(const float (&a)[4]) { return make_float4(a[0], a[1], a[2], a[3]); }
+};
+template <> struct Vec16<double> {
+  typedef double2 type;
+  static constexpr int N = 2;
+  static __device__ __forceinline__ void unpack(const double2& v, double (&a)[2]) { a[0] = v.x; a[1] = v.y; }
+  static __device__ __forceinline__ double2 pack(const double (&a)[2]) { return make_double2(a[0], a[1]); }
+};
+
+// Evict-first streaming: every byte is touched exactly once per launch.
+template <typename T>
+__device__ __forceinline__ void load_vec(const T* p, T (&a)[Vec16<T>::N]) {
+  Vec16<T>::unpack(__ldcs(reinterpret_cast<const typename Vec16<T>::type*>(p)), a);
+}
+template <typename T>
+__device__ __forceinline__ void store_vec(T* p, const T (&a)[Vec16<T>::N]) {
+  __stcs(reinterpret_cast<typename Vec16<T>::type*>(p), Vec16<T>::pack(a));
+}
+
+}  // namespace clipseg

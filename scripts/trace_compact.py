@@ -1,0 +1,72 @@
+"""Per-tile timeline of the compacting kernel (debug build with -DCLIPSEG_TRACE).
+  python scripts/trace_compact.py [--n 100000000]
+Prints percentiles of: claim->compute start, compute time, A publish -> P publish,
+look-back duration, P -> copy start, and the copy wait of each tile."""
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--n", type=int, default=10**8)
+    a = ap.parse_args()
+    import torch
+    import synth
+    from paper_1110_5450_b200 import clipseg
+    L = ctypes.CDLL(os.path.join(ROOT, "build", "libclipseg_trace.so"))
+    P, I64 = ctypes.c_void_p, ctypes.c_int64
+    f = L.clip_segments_compact_f32
+    f.argtypes = [P, I64, I64, ctypes.POINTER(clipseg.clip_window_f32), P, I64, P, I64, P, P, P, ctypes.c_size_t, P]
+    L.clip_trace_read.argtypes = [P, ctypes.c_size_t]
+    L.clip_trace_read.restype = ctypes.c_int
+    L.clip_trace_clear.restype = ctypes.c_int
+    n = a.n
+    planes = clipseg.empty_planes(n, 2, torch.float32)
+    synth.fill_device(planes, synth.UNIFORM, 2, synth.seed_for(5), n)
+    b = clipseg.CompactBuffers(n, 2, torch.float32, with_flags=True)
+    w = clipseg.make_window([0, 0], [1, 1])
+    s = torch.cuda.current_stream().cuda_stream
+    for _ in range(3):
+        L.clip_trace_clear()
+        st = f(planes.data_ptr(), planes.stride(0), n, ctypes.byref(w), b.out.data_ptr(), b.out.stride(0), None, 0,
+               b.flags.data_ptr(), b.count.data_ptr(), b.ws.data_ptr(), b.ws.numel(), s)
+        assert st == 0
+        torch.cuda.synchronize()
+    ntiles = (n + 2047) // 2048
+    buf = np.zeros(min(ntiles, 1 << 19) * 8, dtype=np.uint64)
+    assert L.clip_trace_read(buf.ctypes.data, buf.nbytes) == 0
+    t = buf.reshape(-1, 8).astype(np.int64)
+    t0 = t[:, 0][t[:, 0] > 0].min()
+    tr = t.copy()
+    tr[:, :7] -= t0
+    ok = (t[:, 1] > 0) & (t[:, 2] > 0) & (t[:, 5] > 0) & (t[:, 6] > 0)
+    tr = tr[ok]
+    pct = lambda x: {p: round(float(np.percentile(x, p)) / 1000, 2) for p in (10, 50, 90, 99)}  # noqa: E731
+    res = {
+        "tiles": int(ok.sum()),
+        "span_us": float(tr[:, 6].max()) / 1000,
+        "claim_to_start_us": pct(tr[:, 1] - tr[:, 0]),
+        "compute_us (start->A)": pct(tr[:, 2] - tr[:, 1]),
+        "lookback_us": pct(tr[:, 4] - tr[:, 3]),
+        "lookback_end_minus_A_us": pct(tr[:, 4] - tr[:, 2]),
+        "A_to_P_us (scanner publish)": pct(tr[:, 5] - tr[:, 2]),
+        "P_published_to_seen_us": pct(tr[:, 4] - tr[:, 5]),
+        "poll_start_minus_A_us": pct(tr[:, 3] - tr[:, 2]),
+        "P_seen_to_copy_us": pct(tr[:, 6] - tr[:, 4]),
+        "claim_order_vs_A_order_inversions": float(np.mean(np.diff(tr[:, 2]) < 0)),
+    }
+    # lateness of predecessor: A time of t-1 minus A time of t
+    res["pred_A_later_than_mine_us"] = pct(np.maximum(tr[:-1, 2] - tr[1:, 2], 0))
+    print(json.dumps(res, indent=1))
+
+
+if __name__ == "__main__":
+    main()

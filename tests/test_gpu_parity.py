@@ -1,0 +1,202 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, element by element,
+on the same seeded inputs.  Bar: bit-exact flags, compaction order, counts AND endpoints
+(the kernel executes the same IEEE operations the rules prescribe), which implies the
+north-star tolerances (1e-6 x extent fp32, 1e-14 fp64)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+UNIT = {2: ([0.0, 0.0], [1.0, 1.0]), 3: ([0.0, 0.0, 0.0], [1.0, 1.0, 1.0])}
+# sizes spanning several tiles (1024 / 512 segments) and every ragged tail
+SIZES = [1, 3, 4, 5, 31, 1023, 1024, 1025, 4097, 10007, 100003, 1 << 20]
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch as t  # noqa: PLC0415
+    assert t.cuda.is_available()
+    return t
+
+
+@pytest.fixture(scope="module")
+def cs():
+    from paper_1110_5450_b200 import clipseg  # noqa: PLC0415
+    return clipseg
+
+
+def bits(a):
+    a = np.ascontiguousarray(a)
+    return a.view(np.uint32 if a.dtype == np.float32 else np.uint64)
+
+
+def to_dev(torch, planes):
+    return torch.from_numpy(np.ascontiguousarray(planes)).cuda()
+
+
+def gen(family, dim, seed, n, dtype, mix=(1 / 3, 1 / 3)):
+    pin, pc = synth.mix_thresholds(*mix)
+    planes, tag = synth.fill_host(family, dim, seed, n, dtype=dtype, p_in=pin, p_cross=pc)
+    return planes, tag
+
+
+def check_dense(torch, cs, planes, n, lo, hi, dim):
+    want, wflags = oracle.clip(planes, n, lo, hi, dim, nthreads=8)
+    d_in = to_dev(torch, planes)
+    out, flags = cs.clip(d_in, n, lo, hi)
+    torch.cuda.synchronize()
+    got, gflags = out.cpu().numpy(), flags.cpu().numpy()[:n]
+    assert np.array_equal(gflags, wflags), np.nonzero(gflags != wflags)[0][:10]
+    diff = np.nonzero(np.any(bits(got[:, :n]) != bits(want[:, :n]), axis=0))[0]
+    assert len(diff) == 0, (diff[:5], planes[:, diff[:3]], got[:, diff[:3]], want[:, diff[:3]])
+    return wflags
+
+
+def check_compact(torch, cs, planes, n, lo, hi, dim, index_base=0):
+    want, widx, wcnt, wflags = oracle.compact(planes, n, lo, hi, dim, index_base=index_base, with_flags=True)
+    d_in = to_dev(torch, planes)
+    b = cs.clip_compact(d_in, n, lo, hi, with_index=True, with_flags=True, index_base=index_base)
+    torch.cuda.synchronize()
+    cnt = int(b.count.item())
+    assert cnt == wcnt
+    assert np.array_equal(b.flags.cpu().numpy()[:n], wflags)
+    assert np.array_equal(b.index.cpu().numpy()[:cnt], widx)
+    got = b.out.cpu().numpy()
+    assert np.array_equal(bits(got[:, :cnt]), bits(want[:, :cnt]))
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_dense_2d_f32_uniform_sizes(torch, cs, n):
+    planes, _ = gen(synth.UNIFORM, 2, synth.seed_for(1), n, np.float32)
+    check_dense(torch, cs, planes, n, *UNIT[2], 2)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("family", [synth.UNIFORM, synth.MIX, synth.ADVERSARIAL])
+def test_dense_families(torch, cs, dim, dtype, family):
+    n = 300007
+    planes, _ = gen(family, dim, synth.seed_for(2, family), n, dtype)
+    check_dense(torch, cs, planes, n, *UNIT[dim], dim)
+
+
+@pytest.mark.parametrize("mix", [(0.10, 0.80), (1 / 3, 1 / 3), (0.90, 0.05)])
+def test_dense_mix_sweep_ground_truth(torch, cs, mix):
+    n = 1 << 20
+    planes, tag = gen(synth.MIX, 2, synth.seed_for(2), n, np.float32, mix)
+    flags = check_dense(torch, cs, planes, n, *UNIT[2], 2)
+    assert np.array_equal(flags, (tag != synth.CAT_OUTSIDE).astype(np.uint8))
+
+
+@pytest.mark.parametrize("lo,hi", [([0.25, -0.5], [0.75, 1.25]), ([0.5, 0.5], [0.5, 0.5]), ([-1, -1], [1, 1])])
+def test_dense_other_windows(torch, cs, lo, hi):
+    n = 100003
+    planes, _ = gen(synth.UNIFORM, 2, synth.seed_for(1, 9), n, np.float32)
+    check_dense(torch, cs, planes, n, lo, hi, 2)
+    check_compact(torch, cs, planes, n, lo, hi, 2)
+
+
+def test_dense_nonfinite_inputs(torch, cs):
+    n = 4096
+    planes, _ = gen(synth.UNIFORM, 2, synth.seed_for(1, 10), n, np.float32)
+    rng = np.random.default_rng(0)
+    for v in (np.nan, np.inf, -np.inf):
+        idx = rng.integers(0, n, 50)
+        planes[rng.integers(0, 4, 50), idx] = v
+    check_dense(torch, cs, planes, n, *UNIT[2], 2)
+
+
+def test_dense_in_place(torch, cs):
+    n = 50001
+    planes, _ = gen(synth.UNIFORM, 2, synth.seed_for(1, 11), n, np.float32)
+    want, wflags = oracle.clip(planes, n, *UNIT[2], 2)
+    d = to_dev(torch, planes)
+    out, flags = cs.clip(d, n, *UNIT[2], out=d)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(d.cpu().numpy()[:, :n]), bits(want[:, :n]))
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_compact_2d_f32_sizes(torch, cs, n):
+    planes, _ = gen(synth.UNIFORM, 2, synth.seed_for(5), n, np.float32)
+    check_compact(torch, cs, planes, n, *UNIT[2], 2, index_base=12345)
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("family", [synth.UNIFORM, synth.MIX, synth.ADVERSARIAL])
+def test_compact_families(torch, cs, dim, dtype, family):
+    n = 300007
+    planes, _ = gen(family, dim, synth.seed_for(5, family), n, dtype)
+    check_compact(torch, cs, planes, n, *UNIT[dim], dim)
+
+
+def test_compact_all_and_none_visible(torch, cs):
+    n = 70001
+    pin, pc = synth.mix_thresholds(1.0 - 2**-32, 0.0)
+    planes, _ = synth.fill_host(synth.MIX, 2, 3, n, p_in=pin, p_cross=pc)      # all inside
+    check_compact(torch, cs, planes, n, *UNIT[2], 2)
+    planes, _ = synth.fill_host(synth.MIX, 2, 3, n, p_in=0, p_cross=0)          # all outside
+    check_compact(torch, cs, planes, n, *UNIT[2], 2)
+
+
+def test_compact_zero_n(torch, cs):
+    d = torch.zeros((4, 32), dtype=torch.float32, device="cuda")
+    b = cs.clip_compact(d, 0, *UNIT[2])
+    torch.cuda.synchronize()
+    assert int(b.count.item()) == 0
+
+
+def test_compact_repeat_reuses_workspace(torch, cs):
+    n = 200003
+    planes, _ = gen(synth.UNIFORM, 2, synth.seed_for(5, 3), n, np.float32)
+    d = to_dev(torch, planes)
+    b = cs.clip_compact(d, n, *UNIT[2], with_index=True)
+    first = b.out.clone()
+    for _ in range(3):
+        cs.clip_compact(d, n, *UNIT[2], bufs=b)
+    torch.cuda.synchronize()
+    cnt = int(b.count.item())
+    assert torch.equal(first[:, :cnt], b.out[:, :cnt])
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_host_pipeline(torch, cs, dtype):
+    n = 1000003
+    planes, _ = gen(synth.UNIFORM, 2, synth.seed_for(5, 4), n, dtype)
+    want, _, wcnt, wflags = oracle.compact(planes, n, *UNIT[2], 2, with_flags=True)
+    h_in = torch.from_numpy(planes).pin_memory()
+    h_out = torch.empty_like(h_in).pin_memory()
+    h_flags = torch.empty(n, dtype=torch.uint8).pin_memory()
+    cnt, _ = cs.clip_compact_host(h_in, n, *UNIT[2], h_out, h_flags=h_flags, chunk=300000)
+    assert cnt == wcnt
+    assert np.array_equal(h_flags.numpy(), wflags)
+    assert np.array_equal(bits(h_out.numpy()[:, :cnt]), bits(want[:, :cnt]))
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+@pytest.mark.parametrize("family", [synth.UNIFORM, synth.MIX, synth.ADVERSARIAL])
+def test_generator_device_twin(torch, family, dtype):
+    n = 200003
+    pin, pc = synth.mix_thresholds(0.1, 0.8)
+    host, htag = synth.fill_host(family, 3 if family != synth.ADVERSARIAL else 2, 99, n, dtype=dtype, i0=777,
+                                 p_in=pin, p_cross=pc)
+    d = torch.zeros(host.shape, dtype=torch.float32 if dtype == np.float32 else torch.float64, device="cuda")
+    tag = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    synth.fill_device(d, family, host.shape[0] // 2, 99, n, i0=777, p_in=pin, p_cross=pc, tag_t=tag)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(d.cpu().numpy()[:, :n]), bits(host[:, :n]))
+    assert np.array_equal(tag.cpu().numpy(), htag)
+
+
+def test_shard_offsets_kernel(torch, cs):
+    counts = torch.tensor([5, 0, 7, 11, 3], dtype=torch.int64, device="cuda")
+    for r in range(5):
+        off = cs.shard_offsets(counts, r)
+        torch.cuda.synchronize()
+        assert off.tolist() == [int(counts[:r].sum()), 26]
