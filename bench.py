@@ -110,9 +110,11 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def cpu_oracle_rate(n_sample, nthreads):
-    """The oracle as it stands (oracle/libclip_oracle.so, plain scalar C) on host cores,
-    over the first n_sample segments of the workload; returns (seg/s, seconds, threads)."""
+def cpu_oracle_rate(n_sample, nthreads, min_seconds=10.0):
+    """The oracle as it stands (oracle/libclip_oracle.so, plain scalar C) on host cores.
+    Bounded sample: the first n_sample segments of the workload (regenerated on the host by
+    the same seeded generator), clipped repeatedly until min_seconds of wall time have
+    passed, statically split over nthreads threads.  Returns (seg/s, seconds, threads, passes)."""
     import numpy as np  # noqa: PLC0415
     import oracle  # noqa: PLC0415  (cpu_baseline leg: the one place bench.py runs oracle/)
     import synth  # noqa: PLC0415
@@ -128,15 +130,20 @@ def cpu_oracle_rate(n_sample, nthreads):
         f(DIM, lo3.ctypes.data, hi3.ctypes.data, planes.ctypes.data + 4 * a, ld, b - a, out.ctypes.data + 4 * a,
           ld, flags.ctypes.data + a)
 
+    passes = 0
     t0 = time.perf_counter()
-    ths = [threading.Thread(target=run, args=(n_sample * t // nthreads, n_sample * (t + 1) // nthreads))
-           for t in range(nthreads)]
-    for th in ths:
-        th.start()
-    for th in ths:
-        th.join()
-    dt = time.perf_counter() - t0
-    return n_sample / dt, dt, nthreads
+    while True:
+        ths = [threading.Thread(target=run, args=(n_sample * t // nthreads, n_sample * (t + 1) // nthreads))
+               for t in range(nthreads)]
+        for th in ths:
+            th.start()
+        for th in ths:
+            th.join()
+        passes += 1
+        dt = time.perf_counter() - t0
+        if dt >= min_seconds:
+            break
+    return passes * n_sample / dt, dt, nthreads, passes
 
 
 def host_threads():
@@ -152,11 +159,11 @@ def run_reference(args, rank, world):
         return
     nth = min(host_threads(), 64)
     n_s = args.cpu_sample
-    cpu_oracle_rate(min(n_s, 1_000_000), nth)   # warm-up (page-in, thread start)
+    cpu_oracle_rate(min(n_s, 1_000_000), nth, 0.0)   # warm-up (page-in, thread start)
     rates = []
     total_t = 0.0
     for _ in range(args.steps):
-        r, dt, _ = cpu_oracle_rate(n_s, nth)
+        r, dt, _, passes = cpu_oracle_rate(n_s, nth, 0.0)
         rates.append(r)
         total_t += dt
         if total_t > 120:
@@ -276,9 +283,10 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         nth = min(host_threads(), 64)
-        r, dt, nth = cpu_oracle_rate(args.cpu_sample, nth)
+        r, dt, nth, passes = cpu_oracle_rate(args.cpu_sample, nth, 10.0)
         cpu = {"value": r, "unit": "segments/s", "cores": nth, "kind": "oracle",
-               "sample": f"first {args.cpu_sample} segments of the workload ({dt:.1f} s wall, {nth} threads)"}
+               "sample": f"first {args.cpu_sample} segments of the workload, {passes} passes in {dt:.1f} s "
+                         f"wall on {nth} threads (static split)"}
 
     if world > 1:
         dist.barrier()

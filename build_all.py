@@ -87,6 +87,18 @@ def build_trace():
     return out
 
 
+def build_variant(name, defines, verbose=False):
+    """Experimental build with -D tuning knobs into build/libclipseg_<name>.so."""
+    srcs = _clipseg_sources()
+    out = os.path.join(ROOT, "build", f"libclipseg_{name}.so")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    cus = [os.path.relpath(s, ROOT) for s in srcs if s.endswith(".cu")]
+    extra = ["-Xptxas", "-v"] if verbose else []
+    log = _run([NVCC, *ARCH, *NVCC_FP, *NVCC_COMMON, *extra, *[f"-D{d}" for d in defines], "-Iinclude", *cus,
+                "-o", out])
+    return out, log
+
+
 def build(force=False, verbose=False):
     build_synth(force)
     build_oracle(force)

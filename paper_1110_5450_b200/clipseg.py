@@ -12,7 +12,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libclipseg.so")
+# CLIPSEG_LIB selects an experimental build of the same library (scripts/sweep_*.py)
+LIB_PATH = os.environ.get("CLIPSEG_LIB") or os.path.join(_HERE, "lib", "libclipseg.so")
 
 CLIP_OK, CLIP_EINVAL, CLIP_EALIGN, CLIP_ENOSPACE, CLIP_ECUDA = 0, -1, -2, -3, -4
 

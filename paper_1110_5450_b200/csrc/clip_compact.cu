@@ -158,7 +158,7 @@ template <typename T, int D> struct CompactShape {
   static constexpr int SLOT = 2 * D * SUB;               // staged elements per sub-tile
   static constexpr size_t kStageBytes = (size_t)NBUF * NSUB * SLOT * sizeof(T);
   static constexpr size_t kSmemBytes = kStageBytes + (size_t)NBUF * NSUB * SUB;  // + local indices
-  static constexpr int kMinBlocks = (sizeof(T) == 4 && D == 2) ? 2 : 1;
+  static constexpr int kMinBlocks = compact_min_blocks<T, D>();
 };
 
 template <typename T, int D>

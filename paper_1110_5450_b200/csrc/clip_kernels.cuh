@@ -19,11 +19,23 @@ template <typename T> __host__ __device__ constexpr int vec_elems() { return 16 
 // tiles are staged in shared memory at once (the copy-out lags the compute by that many
 // minus one), sized to stay near 100 KB of shared memory per block.
 template <typename T> __host__ __device__ constexpr int compact_items() { return 4 / vec_elems<T>(); }
+#ifndef CLIPSEG_NSUB_F32_2D  // tuning knobs of the headline (fp32, 2D) instantiation
+#define CLIPSEG_NSUB_F32_2D 16
+#endif
+#ifndef CLIPSEG_NBUF_F32_2D
+#define CLIPSEG_NBUF_F32_2D 3
+#endif
+#ifndef CLIPSEG_MINB_F32_2D
+#define CLIPSEG_MINB_F32_2D 2
+#endif
 template <typename T, int D> __host__ __device__ constexpr int compact_subtiles() {
-  return (sizeof(T) == 4 && D == 2) ? 16 : 8;
+  return (sizeof(T) == 4 && D == 2) ? CLIPSEG_NSUB_F32_2D : 8;
 }
 template <typename T, int D> __host__ __device__ constexpr int compact_buffers() {
-  return (sizeof(T) == 8 && D == 3) ? 2 : 3;
+  return (sizeof(T) == 4 && D == 2) ? CLIPSEG_NBUF_F32_2D : ((sizeof(T) == 8 && D == 3) ? 2 : 3);
+}
+template <typename T, int D> __host__ __device__ constexpr int compact_min_blocks() {
+  return (sizeof(T) == 4 && D == 2) ? CLIPSEG_MINB_F32_2D : 1;
 }
 // Smallest block tile over all (T, D): the workspace is sized with it.
 constexpr int64_t kMinCompactTile = 8 * 128;

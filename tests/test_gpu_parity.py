@@ -200,3 +200,27 @@ def test_shard_offsets_kernel(torch, cs):
         off = cs.shard_offsets(counts, r)
         torch.cuda.synchronize()
         assert off.tolist() == [int(counts[:r].sum()), 26]
+
+
+def test_sharded_compact_single_rank_nccl(torch, cs):
+    """The sharded entry (CUDA compaction + NCCL allgather + offset kernel) at world size 1."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_1110_5450_b200.shard import sharded_compact
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        n = 300007
+        planes, _ = gen(synth.UNIFORM, 2, synth.seed_for(5), n, np.float32)
+        want, widx, wcnt = oracle.compact(planes, n, *UNIT[2], 2, index_base=1000)
+        res, b = sharded_compact(to_dev(torch, planes), n, *UNIT[2], 1000)
+        torch.cuda.synchronize()
+        assert res.offsets.tolist() == [0, wcnt] and res.counts.tolist() == [wcnt]
+        assert np.array_equal(bits(b.out.cpu().numpy()[:, :wcnt]), bits(want[:, :wcnt]))
+        assert np.array_equal(b.index.cpu().numpy()[:wcnt], widx)
+    finally:
+        dist.destroy_process_group()
