@@ -10,10 +10,11 @@
 //    last of its predecessors has published, with no redundant per-tile walks;
 //
 //  * every other block claims block tiles of BT = NSUB x 128 segments in increasing order
-//    from an atomic counter (the first of its compute warps to become free claims, so claim
-//    order follows the order blocks start computing) and runs
+//    from an atomic counter (the first of its compute warps to start a tile claims the
+//    block's next one, so claims follow the order blocks start computing) and runs
 //      - 8 compute warps.  Per sub-tile (32 lanes x 4 segments, one 128-bit load per plane
-//        per lane, the next sub-tile's loads in flight while this one is clipped) a warp
+//        per lane; the next sub-tile's loads — across tile boundaries — in flight while this
+//        one is clipped) a warp
 //        classifies and clips its segments (clip_math.cuh), stores the flags, warp-scans the
 //        visible counts and stages the visible rows, compacted, in its slot of stage buffer
 //        k % NBUF.  The last warp to finish a tile publishes its aggregate (flag A).  Then
@@ -257,59 +258,66 @@ __global__ void __launch_bounds__(kThreads, CompactShape<T, D>::kMinBlocks) clip
   }
   int b = 0;
   unsigned par = 0;
-  bool claiming = true;
-  for (int64_t k = 0;; ++k) {
-    int64_t tile = ntiles;
-    if (claiming) {
-      if (k > 0 && lane == 0) {
-        // the first compute warp to reach tile k claims it
-        const int order = atomicAdd(&s_claim[k & 3], 1);
-        if (order == 0) {
-          s_tile[k & 3] = (int64_t)atomicAdd(counter, 1ull);
-          CLIP_TRACE(s_tile[k & 3], 0, trace_now());
-          mbar_arrive(&mb_tile[k & 3]);
-        } else if (order == kComputeWarps - 1) {
-          s_claim[k & 3] = 0;  // every warp has passed this slot; reused at iteration k + 4
-        }
+  // segments of sub-tile `sub` of tile t still in range (SUB for every full sub-tile)
+  auto remaining = [&](int64_t t, int sub) -> int {
+    const int64_t r = n - (t * BT + (int64_t)sub * SUB);
+    return r >= SUB ? SUB : (r > 0 ? (int)r : 0);
+  };
+  auto load = [&](int64_t t, int sub, T (&dst)[IT][2 * D][V]) {
+    const T* src = in + t * BT + (int64_t)sub * SUB;
+    const int rem = remaining(t, sub);
+#pragma unroll
+    for (int j = 0; j < IT; ++j) {
+      const int o = (32 * j + lane) * V;
+      if (o < rem) {
+#pragma unroll
+        for (int c = 0; c < 2 * D; ++c) load_vec<T>(src + c * ld_in + o, dst[j][c]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 2 * D; ++c)
+#pragma unroll
+          for (int v = 0; v < V; ++v) dst[j][c][v] = T(0);
       }
-      mbar_wait(&mb_tile[k & 3], (uint32_t)((k >> 2) & 1));
-      tile = s_tile[k & 3];
-      if (tile >= ntiles) claiming = false;
+    }
+  };
+  // Sub-tile loads run one ahead of the clipping, across tile boundaries: the next tile is
+  // claimed as this one starts, and its first sub-tile is loaded during this one's last.
+  T buf[2][IT][2 * D][V];
+  mbar_wait(&mb_tile[0], 0u);
+  int64_t tile = s_tile[0];
+  if (tile < ntiles) load(tile, warp, buf[0]);
+  for (int64_t k = 0;; ++k) {
+    int64_t next = ntiles;
+    if (tile < ntiles && lane == 0) {
+      // the first compute warp to start tile k claims the tile of iteration k + 1
+      const int q = (int)((k + 1) & 3);
+      const int order = atomicAdd(&s_claim[q], 1);
+      if (order == 0) {
+        s_tile[q] = (int64_t)atomicAdd(counter, 1ull);
+        CLIP_TRACE(s_tile[q], 0, trace_now());
+        mbar_arrive(&mb_tile[q]);
+      } else if (order == kComputeWarps - 1) {
+        s_claim[q] = 0;  // every warp has passed this slot; reused at iteration k + 5
+      }
     }
     if (tile < ntiles) {
       if (warp == 0 && lane == 0) CLIP_TRACE(tile, 1, trace_now());
       T* stg = stage + (size_t)b * NSUB * SLOT;
       uint8_t* lix = lidx + (size_t)b * NSUB * SUB;
-      // segments of sub-tile `sub` still in range (SUB for every full sub-tile)
-      auto remaining = [&](int sub) -> int {
-        const int64_t r = n - (tile * BT + (int64_t)sub * SUB);
-        return r >= SUB ? SUB : (r > 0 ? (int)r : 0);
-      };
-      auto load = [&](int sub, T (&dst)[IT][2 * D][V]) {
-        const T* src = in + tile * BT + (int64_t)sub * SUB;
-        const int rem = remaining(sub);
-#pragma unroll
-        for (int j = 0; j < IT; ++j) {
-          const int o = (32 * j + lane) * V;
-          if (o < rem) {
-#pragma unroll
-            for (int c = 0; c < 2 * D; ++c) load_vec<T>(src + c * ld_in + o, dst[j][c]);
-          } else {
-#pragma unroll
-            for (int c = 0; c < 2 * D; ++c)
-#pragma unroll
-              for (int v = 0; v < V; ++v) dst[j][c][v] = T(0);
-          }
-        }
-      };
-      T buf[2][IT][2 * D][V];
-      load(warp, buf[0]);  // sub-tile loads run one ahead of the clipping
 #pragma unroll
       for (int r = 0; r < PER_WARP; ++r) {
         const int sub = r * kComputeWarps + warp;
-        if (r + 1 < PER_WARP) load(sub + kComputeWarps, buf[(r + 1) & 1]);
-        const T (&plane)[IT][2 * D][V] = buf[r & 1];
-        const int rem = remaining(sub);
+        // buf[(k*PER_WARP + r) & 1] holds this sub-tile; load the next one into the other
+        const int cur = (int)((k * PER_WARP + r) & 1);
+        if (r + 1 < PER_WARP) {
+          load(tile, sub + kComputeWarps, buf[cur ^ 1]);
+        } else {
+          mbar_wait(&mb_tile[(k + 1) & 3], (uint32_t)(((k + 1) >> 2) & 1));
+          next = s_tile[(k + 1) & 3];
+          if (next < ntiles) load(next, warp, buf[cur ^ 1]);
+        }
+        const T (&plane)[IT][2 * D][V] = buf[cur];
+        const int rem = remaining(tile, sub);
         uint8_t* fl = flags ? flags + tile * BT + (int64_t)sub * SUB : nullptr;
         T res[IT][2 * D][V];
         unsigned vis[IT];
@@ -429,7 +437,8 @@ __global__ void __launch_bounds__(kThreads, CompactShape<T, D>::kMinBlocks) clip
     ppar[0] = (par >> b) & 1u;
     if (tile < ntiles) par ^= 1u << b;
     b = (b + 1 == NBUF) ? 0 : b + 1;
-    if (!claiming) {
+    tile = next;
+    if (tile >= ntiles) {
       bool any = false;
 #pragma unroll
       for (int q = 0; q <= Q; ++q) any |= pend[q] < ntiles;

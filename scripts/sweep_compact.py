@@ -14,8 +14,8 @@ VARIANTS = {
     "s16b2m3": ["CLIPSEG_NSUB_F32_2D=16", "CLIPSEG_NBUF_F32_2D=2", "CLIPSEG_MINB_F32_2D=3"],
     "s8b4m3": ["CLIPSEG_NSUB_F32_2D=8", "CLIPSEG_NBUF_F32_2D=4", "CLIPSEG_MINB_F32_2D=3"],
     "s8b3m3": ["CLIPSEG_NSUB_F32_2D=8", "CLIPSEG_NBUF_F32_2D=3", "CLIPSEG_MINB_F32_2D=3"],
-    "s16b4m1": ["CLIPSEG_NSUB_F32_2D=16", "CLIPSEG_NBUF_F32_2D=4", "CLIPSEG_MINB_F32_2D=1"],
     "s8b4m2": ["CLIPSEG_NSUB_F32_2D=8", "CLIPSEG_NBUF_F32_2D=4", "CLIPSEG_MINB_F32_2D=2"],
+    "s24b2m2": ["CLIPSEG_NSUB_F32_2D=24", "CLIPSEG_NBUF_F32_2D=2", "CLIPSEG_MINB_F32_2D=2"],
 }
 
 
