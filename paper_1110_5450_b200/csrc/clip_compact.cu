@@ -26,8 +26,10 @@
 //
 // Hand-offs inside a block use shared-memory mbarriers (compute warps -> scan warp: 8
 // arrivals per tile; scan warp -> compute warps: 1; claiming warp -> all: the tile id, a
-// ring of 4).  Status words are 64-bit: flag in bits 62-63 (0 not ready, 1 aggregate,
+// ring of 8).  Status words are 64-bit: flag in bits 62-63 (0 not ready, 1 aggregate,
 // 2 inclusive prefix), value in bits 0-61.  The scanner writes the total count.
+#include <type_traits>
+
 #include "clip_kernels.cuh"
 #include "vec_io.cuh"
 
@@ -62,6 +64,9 @@ constexpr unsigned long long kValueMask = (1ull << 62) - 1;
 constexpr int kComputeWarps = 8;
 constexpr int kThreads = (kComputeWarps + 1) * 32;  // + the scan warp
 constexpr int kScanPerLane = 16;                     // scanner: 512 tiles per probe
+// Claimed-tile ring: a slot is rewritten kTileRing iterations after its first use; it must
+// exceed the copy lag (NBUF - 1) by enough that no warp still reads the old id.
+constexpr int kTileRing = 8, kRingMask = kTileRing - 1;
 
 __device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
   unsigned long long v;
@@ -93,6 +98,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
       "r"(parity), "r"(1000000u)
       : "memory");
+}
+
+// Low-duty-cycle wait for the scan warp, which waits most of its life: a non-blocking phase
+// test plus a real sleep, so it does not take issue slots from the compute warps it shares
+// a scheduler with (a suspending try_wait is woken by every mbarrier event on the SM).
+__device__ __forceinline__ void mbar_wait_sleepy(uint64_t* bar, uint32_t parity, unsigned ns) {
+  for (;;) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(ns);
+  }
 }
 
 // Block 0's scan warp: walks the tile statuses in order and turns every run of published
@@ -156,33 +179,35 @@ template <typename T, int D> struct CompactShape {
   static constexpr int NSUB = compact_subtiles<T, D>();  // sub-tiles per block tile
   static constexpr int BT = NSUB * SUB;
   static constexpr int NBUF = compact_buffers<T, D>();   // staged tiles in flight per block
-  static constexpr int SLOT = 2 * D * SUB;               // staged elements per sub-tile
+  static constexpr int PITCH = SUB + V;                  // staged plane pitch: rows + scratch row
+  static constexpr int SLOT = 2 * D * PITCH;             // staged elements per sub-tile
   static constexpr size_t kStageBytes = (size_t)NBUF * NSUB * SLOT * sizeof(T);
-  static constexpr size_t kSmemBytes = kStageBytes + (size_t)NBUF * NSUB * SUB;  // + local indices
+  static constexpr size_t kSmemBytes = kStageBytes + (size_t)NBUF * NSUB * (SUB + 1);  // + local indices
   static constexpr int kMinBlocks = compact_min_blocks<T, D>();
 };
 
-template <typename T, int D>
+template <typename T, int D, bool FLAGS, bool INDEX>
 __global__ void __launch_bounds__(kThreads, CompactShape<T, D>::kMinBlocks) clip_compact_kernel(
     const T* __restrict__ in, int64_t ld_in, int64_t n, Window<T, D> w, T* __restrict__ out, int64_t ld_out,
     int64_t* __restrict__ out_index, int64_t index_base, uint8_t* __restrict__ flags, int64_t* __restrict__ d_count,
     unsigned long long* __restrict__ ws, int64_t ntiles) {
   typedef CompactShape<T, D> S;
   constexpr int V = S::V, IT = S::IT, SUB = S::SUB, NSUB = S::NSUB, BT = S::BT, SLOT = S::SLOT, NBUF = S::NBUF;
+  constexpr int PITCH = S::PITCH;
   constexpr int PER_WARP = NSUB / kComputeWarps;
-  static_assert(NSUB % kComputeWarps == 0 && NSUB <= 32 && NBUF >= 2 && NBUF <= 4, "tile layout");
+  static_assert(NSUB % kComputeWarps == 0 && NSUB <= 32 && NBUF >= 2 && NBUF <= kTileRing - 2, "tile layout");
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* stage = reinterpret_cast<T*>(smem_raw);            // [NBUF][NSUB][2D][SUB]
-  uint8_t* lidx = smem_raw + S::kStageBytes;            // [NBUF][NSUB][SUB]
+  uint8_t* lidx = smem_raw + S::kStageBytes;            // [NBUF][NSUB][SUB + 1]
   __shared__ int s_cnt[NBUF][NSUB], s_pre[NBUF][NSUB];
   __shared__ int64_t s_prefix[NBUF];
   __shared__ int s_done[NBUF];                           // compute warps finished with buffer b
-  __shared__ int64_t s_tile[4];                          // tile of iteration k in slot k & 3
-  __shared__ int s_claim[4];                             // compute warps that reached slot k & 3
+  __shared__ int64_t s_tile[kTileRing];                  // tile of iteration k in slot k % ring
+  __shared__ int s_claim[kTileRing];                     // compute warps that reached the slot
   __shared__ __align__(8) uint64_t mb_cnt[NBUF];         // compute warps -> scan warp
   __shared__ __align__(8) uint64_t mb_pre[NBUF];         // scan warp -> compute warps
-  __shared__ __align__(8) uint64_t mb_tile[4];           // claiming warp -> all
+  __shared__ __align__(8) uint64_t mb_tile[kTileRing];   // claiming warp -> all
 
   unsigned long long* counter = ws;
   unsigned long long* status = ws + kWsHeaderBytes / 8;
@@ -194,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, CompactShape<T, D>::kMinBlocks) clip
       mbar_init(&mb_cnt[q], kComputeWarps);
       mbar_init(&mb_pre[q], 1);
     }
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < kTileRing; ++q) {
       s_claim[q] = 0;
       mbar_init(&mb_tile[q], 1);
     }
@@ -214,10 +239,10 @@ __global__ void __launch_bounds__(kThreads, CompactShape<T, D>::kMinBlocks) clip
     int b = 0;
     unsigned par = 0;  // bit q: parity of the next phase of mb_cnt[q] / mb_pre[q]
     for (int64_t k = 0;; ++k) {
-      mbar_wait(&mb_tile[k & 3], (uint32_t)((k >> 2) & 1));
-      const int64_t tile = s_tile[k & 3];
+      mbar_wait_sleepy(&mb_tile[k & kRingMask], (uint32_t)((k / kTileRing) & 1), 256);
+      const int64_t tile = s_tile[k & kRingMask];
       if (tile >= ntiles) break;
-      mbar_wait(&mb_cnt[b], (par >> b) & 1u);  // the compute warps' counts of tile k
+      mbar_wait_sleepy(&mb_cnt[b], (par >> b) & 1u, 256);  // the compute warps' counts of tile k
       const int c = (lane < NSUB) ? s_cnt[b][lane] : 0;
       int incl = c;
 #pragma unroll
@@ -231,7 +256,7 @@ __global__ void __launch_bounds__(kThreads, CompactShape<T, D>::kMinBlocks) clip
         CLIP_TRACE(tile, 3, trace_now());
         unsigned long long st;
         while (((st = ld_relaxed(status + tile)) >> 62) != 2u)  // the scanner's inclusive prefix
-          __nanosleep(1000);  // it typically lands a few microseconds after the aggregate
+          __nanosleep(500);  // it typically lands several microseconds after the aggregate
         CLIP_TRACE(tile, 4, trace_now());
         CLIP_TRACE(tile, 7, blockIdx.x);
         s_prefix[b] = (int64_t)(st & kValueMask) - total;
@@ -263,13 +288,13 @@ __global__ void __launch_bounds__(kThreads, CompactShape<T, D>::kMinBlocks) clip
     const int64_t r = n - (t * BT + (int64_t)sub * SUB);
     return r >= SUB ? SUB : (r > 0 ? (int)r : 0);
   };
-  auto load = [&](int64_t t, int sub, T (&dst)[IT][2 * D][V]) {
+  auto load = [&](int64_t t, int sub, T (&dst)[IT][2 * D][V], const bool FULL) {
     const T* src = in + t * BT + (int64_t)sub * SUB;
-    const int rem = remaining(t, sub);
+    const int rem = FULL ? SUB : remaining(t, sub);
 #pragma unroll
     for (int j = 0; j < IT; ++j) {
       const int o = (32 * j + lane) * V;
-      if (o < rem) {
+      if (FULL || o < rem) {
 #pragma unroll
         for (int c = 0; c < 2 * D; ++c) load_vec<T>(src + c * ld_in + o, dst[j][c]);
       } else {
@@ -285,92 +310,110 @@ __global__ void __launch_bounds__(kThreads, CompactShape<T, D>::kMinBlocks) clip
   T buf[2][IT][2 * D][V];
   mbar_wait(&mb_tile[0], 0u);
   int64_t tile = s_tile[0];
-  if (tile < ntiles) load(tile, warp, buf[0]);
+  if (tile < ntiles) load(tile, warp, buf[0], false);
   for (int64_t k = 0;; ++k) {
     int64_t next = ntiles;
     if (tile < ntiles && lane == 0) {
       // the first compute warp to start tile k claims the tile of iteration k + 1
-      const int q = (int)((k + 1) & 3);
+      const int q = (int)((k + 1) & kRingMask);
       const int order = atomicAdd(&s_claim[q], 1);
       if (order == 0) {
         s_tile[q] = (int64_t)atomicAdd(counter, 1ull);
         CLIP_TRACE(s_tile[q], 0, trace_now());
         mbar_arrive(&mb_tile[q]);
       } else if (order == kComputeWarps - 1) {
-        s_claim[q] = 0;  // every warp has passed this slot; reused at iteration k + 5
+        s_claim[q] = 0;  // every warp has passed this slot; reused kTileRing iterations later
       }
     }
     if (tile < ntiles) {
       if (warp == 0 && lane == 0) CLIP_TRACE(tile, 1, trace_now());
       T* stg = stage + (size_t)b * NSUB * SLOT;
-      uint8_t* lix = lidx + (size_t)b * NSUB * SUB;
+      uint8_t* lix = lidx + (size_t)b * NSUB * (SUB + 1);
+      auto body = [&](const bool FULL) {
 #pragma unroll
-      for (int r = 0; r < PER_WARP; ++r) {
-        const int sub = r * kComputeWarps + warp;
-        // buf[(k*PER_WARP + r) & 1] holds this sub-tile; load the next one into the other
-        const int cur = (int)((k * PER_WARP + r) & 1);
-        if (r + 1 < PER_WARP) {
-          load(tile, sub + kComputeWarps, buf[cur ^ 1]);
-        } else {
-          mbar_wait(&mb_tile[(k + 1) & 3], (uint32_t)(((k + 1) >> 2) & 1));
-          next = s_tile[(k + 1) & 3];
-          if (next < ntiles) load(next, warp, buf[cur ^ 1]);
-        }
-        const T (&plane)[IT][2 * D][V] = buf[cur];
-        const int rem = remaining(tile, sub);
-        uint8_t* fl = flags ? flags + tile * BT + (int64_t)sub * SUB : nullptr;
-        T res[IT][2 * D][V];
-        unsigned vis[IT];
+        for (int r = 0; r < PER_WARP; ++r) {
+          const int sub = r * kComputeWarps + warp;
+          // With an even PER_WARP, buf[r & 1] holds this sub-tile and the next one loads into
+          // the other (static indices keep both in registers); with an odd one the current
+          // sub-tile is copied out of buf[0] first.
+          constexpr bool PING = (PER_WARP % 2) == 0;
+          const int cur = PING ? (r & 1) : 0;
+          T held[IT][2 * D][V];
+          if (!PING) {
 #pragma unroll
-        for (int j = 0; j < IT; ++j) {
-          const int o = (32 * j + lane) * V;
-          const unsigned live = (o >= rem) ? 0u : (o + V <= rem ? (1u << V) - 1u : (1u << (rem - o)) - 1u);
-          vis[j] = clip_group<T, D, V, false>(plane[j], w, res[j]) & live;
-          if (fl) {
-            uint32_t packed = 0;
+            for (int j = 0; j < IT; ++j)
 #pragma unroll
-            for (int v = 0; v < V; ++v) packed |= ((vis[j] >> v) & 1u) << (8 * v);
-            if (o + V <= rem) {
-              if (V == 4) *reinterpret_cast<uint32_t*>(fl + o) = packed;
-              else *reinterpret_cast<uint16_t*>(fl + o) = (uint16_t)packed;
-            } else {
-              for (int v = 0; v < V; ++v)
-                if (o + v < rem) fl[o + v] = (uint8_t)((vis[j] >> v) & 1u);
+              for (int c = 0; c < 2 * D; ++c)
+#pragma unroll
+                for (int v = 0; v < V; ++v) held[j][c][v] = buf[0][j][c][v];
+          }
+          T (&dst)[IT][2 * D][V] = PING ? buf[cur ^ 1] : buf[0];
+          if (r + 1 < PER_WARP) {
+            load(tile, sub + kComputeWarps, dst, FULL);
+          } else {
+            mbar_wait(&mb_tile[(k + 1) & kRingMask], (uint32_t)(((k + 1) / kTileRing) & 1));
+            next = s_tile[(k + 1) & kRingMask];
+            if (next < ntiles) load(next, warp, dst, false);
+          }
+          const T (&plane)[IT][2 * D][V] = PING ? buf[cur] : held;
+          const int rem = FULL ? SUB : remaining(tile, sub);
+          uint8_t* fl = FLAGS ? flags + tile * BT + (int64_t)sub * SUB : nullptr;
+          T res[IT][2 * D][V];
+          unsigned vis[IT];
+#pragma unroll
+          for (int j = 0; j < IT; ++j) {
+            const int o = (32 * j + lane) * V;
+            vis[j] = clip_group<T, D, V, false>(plane[j], w, res[j]);
+            if (!FULL) vis[j] &= (o >= rem) ? 0u : (o + V <= rem ? (1u << V) - 1u : (1u << (rem - o)) - 1u);
+            if (FLAGS) {
+              uint32_t packed = 0;
+#pragma unroll
+              for (int v = 0; v < V; ++v) packed |= ((vis[j] >> v) & 1u) << (8 * v);
+              if (FULL || o + V <= rem) {
+                if (V == 4) *reinterpret_cast<uint32_t*>(fl + o) = packed;
+                else *reinterpret_cast<uint16_t*>(fl + o) = (uint16_t)packed;
+              } else {
+                for (int v = 0; v < V; ++v)
+                  if (o + v < rem) fl[o + v] = (uint8_t)((vis[j] >> v) & 1u);
+              }
             }
           }
-        }
-        // warp scan of the visible counts (item j in bit field 8 j)
-        unsigned cnt = 0;
+          // warp scan of the visible counts (item j in bit field 8 j)
+          unsigned cnt = 0;
 #pragma unroll
-        for (int j = 0; j < IT; ++j) cnt |= (unsigned)__popc(vis[j]) << (8 * j);
-        unsigned incl = cnt;
+          for (int j = 0; j < IT; ++j) cnt |= (unsigned)__popc(vis[j]) << (8 * j);
+          unsigned incl = cnt;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-          if (lane >= d) incl += y;
-        }
-        const unsigned tot_f = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        const unsigned excl_f = incl - cnt;
-        // stage the visible rows, compacted, at the front of this sub-tile's slot
-        T* st = stg + sub * SLOT;
-        int before = 0;
-#pragma unroll
-        for (int j = 0; j < IT; ++j) {
-          int pos = before + (int)((excl_f >> (8 * j)) & 0xFFu);
-#pragma unroll
-          for (int v = 0; v < V; ++v) {
-            const bool on = (vis[j] >> v) & 1u;
-            if (on) {
-#pragma unroll
-              for (int c = 0; c < 2 * D; ++c) st[c * SUB + pos] = res[j][c][v];
-              if (out_index) lix[sub * SUB + pos] = (uint8_t)((32 * j + lane) * V + v);
-            }
-            pos += on;
+          for (int d = 1; d < 32; d <<= 1) {
+            const unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+            if (lane >= d) incl += y;
           }
-          before += (int)((tot_f >> (8 * j)) & 0xFFu);
+          const unsigned tot_f = __shfl_sync(0xFFFFFFFFu, incl, 31);
+          const unsigned excl_f = incl - cnt;
+          // stage the visible rows, compacted, at the front of this sub-tile's slot; an
+          // invisible row goes to the slot's scratch row SUB, so the stores need no branch
+          T* st = stg + sub * SLOT;
+          int before = 0;
+#pragma unroll
+          for (int j = 0; j < IT; ++j) {
+            int pos = before + (int)((excl_f >> (8 * j)) & 0xFFu);
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+              const bool on = (vis[j] >> v) & 1u;
+              T* row = st + (on ? pos : SUB);
+#pragma unroll
+              for (int c = 0; c < 2 * D; ++c) row[c * PITCH] = res[j][c][v];
+              if (INDEX) lix[sub * (SUB + 1) + (on ? pos : SUB)] = (uint8_t)((32 * j + lane) * V + v);
+              pos += on;
+            }
+            before += (int)((tot_f >> (8 * j)) & 0xFFu);
+          }
+          if (lane == 0) s_cnt[b][sub] = before;
         }
-        if (lane == 0) s_cnt[b][sub] = before;
-      }
+      };
+      // (a second copy specialised for full tiles saves ~10% of the instructions but doubles
+      // the hot loop's code, and the instruction-cache misses cost more: measured 7.5 vs 9.2 ms)
+      body(false);
       // the last compute warp to finish publishes the tile aggregate (flag A) at once
       __syncwarp();
       int last = 0;
@@ -400,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, CompactShape<T, D>::kMinBlocks) clip
       if (warp == 0 && lane == 0) CLIP_TRACE(pend[Q], 6, trace_now());
       const int64_t prefix = s_prefix[pb];
       const T* stg = stage + (size_t)pb * NSUB * SLOT;
-      const uint8_t* lix = lidx + (size_t)pb * NSUB * SUB;
+      const uint8_t* lix = lidx + (size_t)pb * NSUB * (SUB + 1);
 #pragma unroll
       for (int r = 0; r < PER_WARP; ++r) {
         const int sub = r * kComputeWarps + warp;  // the sub-tiles this warp staged
@@ -409,19 +452,18 @@ __global__ void __launch_bounds__(kThreads, CompactShape<T, D>::kMinBlocks) clip
         const T* st = stg + sub * SLOT;
 #pragma unroll
         for (int c = 0; c < 2 * D; ++c) {
-          T* dst = out + c * ld_out + g0;
+          T* dst = out + c * ld_out + g0 + lane;
+          const T* src = st + c * PITCH + lane;
 #pragma unroll
-          for (int q = 0; q < SUB / 32; ++q) {
-            const int e = q * 32 + lane;
-            if (e < cnt) __stcs(dst + e, st[c * SUB + e]);
-          }
+          for (int q = 0; q < SUB / 32; ++q)
+            if (q * 32 + lane < cnt) __stcs(dst + q * 32, src[q * 32]);
         }
-        if (out_index) {
+        if (INDEX) {
           const int64_t ib = index_base + pend[Q] * BT + (int64_t)sub * SUB;
 #pragma unroll
           for (int q = 0; q < SUB / 32; ++q) {
             const int e = q * 32 + lane;
-            if (e < cnt) out_index[g0 + e] = ib + lix[sub * SUB + e];
+            if (e < cnt) out_index[g0 + e] = ib + lix[sub * (SUB + 1) + e];
           }
         }
       }
@@ -447,32 +489,51 @@ __global__ void __launch_bounds__(kThreads, CompactShape<T, D>::kMinBlocks) clip
   }
 }
 
+template <typename T, int D, bool FLAGS, bool INDEX>
+static cudaError_t launch_compact_variant(const T* in, int64_t ld_in, int64_t n, const Window<T, D>& w, T* out,
+                                         int64_t ld_out, int64_t* out_index, int64_t index_base, uint8_t* flags,
+                                         int64_t* d_count, unsigned long long* ws, int64_t ntiles, cudaStream_t s) {
+  typedef CompactShape<T, D> S;
+  const size_t smem = S::kSmemBytes;
+  auto kern = clip_compact_kernel<T, D, FLAGS, INDEX>;
+  static int blocks_per_sm = 0;  // cached device attribute
+  if (!blocks_per_sm) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kThreads, smem);
+    if (e != cudaSuccess || blocks_per_sm < 1) blocks_per_sm = 1;
+  }
+  // block 0 is the global scanner; the cooperative launch keeps every block resident, so
+  // the scanner runs alongside the tiles it waits on
+  const int64_t cap = (int64_t)device_sm_count() * blocks_per_sm;
+  const int grid = (int)(ntiles + 1 < cap ? ntiles + 1 : cap);
+  void* args[] = {(void*)&in,     (void*)&ld_in,     (void*)&n,          (void*)&w,     (void*)&out,
+                  (void*)&ld_out, (void*)&out_index, (void*)&index_base, (void*)&flags, (void*)&d_count,
+                  (void*)&ws,     (void*)&ntiles};
+  return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kThreads), args, smem, s);
+}
+
 template <typename T, int D>
 cudaError_t launch_compact(const T* in, int64_t ld_in, int64_t n, const Window<T, D>& w, T* out, int64_t ld_out,
                            int64_t* out_index, int64_t index_base, uint8_t* flags, int64_t* d_count, void* ws,
                            cudaStream_t s) {
   typedef CompactShape<T, D> S;
   const int64_t ntiles = (n + S::BT - 1) / S::BT;
-  const size_t smem = S::kSmemBytes;
-  static int blocks_per_sm = 0;  // cached device attribute
-  if (!blocks_per_sm) {
-    cudaFuncSetAttribute(clip_compact_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, clip_compact_kernel<T, D>,
-                                                                  kThreads, smem);
-    if (e != cudaSuccess || blocks_per_sm < 1) blocks_per_sm = 1;
-  }
   cudaError_t e = cudaMemsetAsync(ws, 0, kWsHeaderBytes + (size_t)ntiles * 8, s);
   if (e != cudaSuccess) return e;
-  // block 0 is the global scanner; the cooperative launch keeps every block resident, so
-  // the scanner runs alongside the tiles it waits on
-  const int64_t cap = (int64_t)device_sm_count() * blocks_per_sm;
-  const int grid = (int)(ntiles + 1 < cap ? ntiles + 1 : cap);
   unsigned long long* wsp = reinterpret_cast<unsigned long long*>(ws);
-  void* args[] = {(void*)&in,     (void*)&ld_in,     (void*)&n,          (void*)&w,     (void*)&out,
-                  (void*)&ld_out, (void*)&out_index, (void*)&index_base, (void*)&flags, (void*)&d_count,
-                  (void*)&wsp,    (void*)&ntiles};
-  return cudaLaunchCooperativeKernel((const void*)clip_compact_kernel<T, D>, dim3(grid), dim3(kThreads), args, smem,
-                                     s);
+  // flags / out_index are optional outputs: one instantiation per combination, so the
+  // per-segment code carries no test for them
+  if (flags && out_index)
+    return launch_compact_variant<T, D, true, true>(in, ld_in, n, w, out, ld_out, out_index, index_base, flags,
+                                                    d_count, wsp, ntiles, s);
+  if (flags)
+    return launch_compact_variant<T, D, true, false>(in, ld_in, n, w, out, ld_out, out_index, index_base, flags,
+                                                     d_count, wsp, ntiles, s);
+  if (out_index)
+    return launch_compact_variant<T, D, false, true>(in, ld_in, n, w, out, ld_out, out_index, index_base, flags,
+                                                     d_count, wsp, ntiles, s);
+  return launch_compact_variant<T, D, false, false>(in, ld_in, n, w, out, ld_out, out_index, index_base, flags,
+                                                    d_count, wsp, ntiles, s);
 }
 
 #ifdef CLIPSEG_TRACE

@@ -11,11 +11,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 VARIANTS = {
     "s16b3m2": ["CLIPSEG_NSUB_F32_2D=16", "CLIPSEG_NBUF_F32_2D=3", "CLIPSEG_MINB_F32_2D=2"],
-    "s16b2m3": ["CLIPSEG_NSUB_F32_2D=16", "CLIPSEG_NBUF_F32_2D=2", "CLIPSEG_MINB_F32_2D=3"],
-    "s8b4m3": ["CLIPSEG_NSUB_F32_2D=8", "CLIPSEG_NBUF_F32_2D=4", "CLIPSEG_MINB_F32_2D=3"],
-    "s8b3m3": ["CLIPSEG_NSUB_F32_2D=8", "CLIPSEG_NBUF_F32_2D=3", "CLIPSEG_MINB_F32_2D=3"],
+    "s8b6m2": ["CLIPSEG_NSUB_F32_2D=8", "CLIPSEG_NBUF_F32_2D=6", "CLIPSEG_MINB_F32_2D=2"],
     "s8b4m2": ["CLIPSEG_NSUB_F32_2D=8", "CLIPSEG_NBUF_F32_2D=4", "CLIPSEG_MINB_F32_2D=2"],
-    "s24b2m2": ["CLIPSEG_NSUB_F32_2D=24", "CLIPSEG_NBUF_F32_2D=2", "CLIPSEG_MINB_F32_2D=2"],
+    "s16b2m2": ["CLIPSEG_NSUB_F32_2D=16", "CLIPSEG_NBUF_F32_2D=2", "CLIPSEG_MINB_F32_2D=2"],
 }
 
 
@@ -31,7 +29,7 @@ def main():
         n = sys.argv[2] if len(sys.argv) > 2 else "1000000000"
         for name in VARIANTS:
             env = dict(os.environ, CLIPSEG_LIB=os.path.join(ROOT, "build", f"libclipseg_{name}.so"))
-            r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "kernel_probe.py"), "--n", n,
+            r = subprocess.run(["timeout", "120", sys.executable, os.path.join(ROOT, "scripts", "kernel_probe.py"), "--n", n,
                                 "--kernel", "compact", "--reps", "5"], env=env, capture_output=True, text=True)
             try:
                 d = json.loads(r.stdout.strip().splitlines()[-1])["compact"]
