@@ -61,8 +61,6 @@ namespace {
 constexpr unsigned long long kFlagA = 1ull << 62;
 constexpr unsigned long long kFlagP = 2ull << 62;
 constexpr unsigned long long kValueMask = (1ull << 62) - 1;
-constexpr int kComputeWarps = 8;
-constexpr int kThreads = (kComputeWarps + 1) * 32;  // + the scan warp
 constexpr int kScanPerLane = 16;                     // scanner: 512 tiles per probe
 // Claimed-tile ring: a slot is rewritten kTileRing iterations after its first use; it must
 // exceed the copy lag (NBUF - 1) by enough that no warp still reads the old id.
@@ -184,16 +182,19 @@ template <typename T, int D> struct CompactShape {
   static constexpr size_t kStageBytes = (size_t)NBUF * NSUB * SLOT * sizeof(T);
   static constexpr size_t kSmemBytes = kStageBytes + (size_t)NBUF * NSUB * (SUB + 1);  // + local indices
   static constexpr int kMinBlocks = compact_min_blocks<T, D>();
+  static constexpr int kComputeWarps = compact_warps<T, D>();
+  static constexpr int kThreads = (kComputeWarps + 1) * 32;  // + the scan warp
 };
 
 template <typename T, int D, bool FLAGS, bool INDEX>
-__global__ void __launch_bounds__(kThreads, CompactShape<T, D>::kMinBlocks) clip_compact_kernel(
+__global__ void __launch_bounds__(CompactShape<T, D>::kThreads, CompactShape<T, D>::kMinBlocks) clip_compact_kernel(
     const T* __restrict__ in, int64_t ld_in, int64_t n, Window<T, D> w, T* __restrict__ out, int64_t ld_out,
     int64_t* __restrict__ out_index, int64_t index_base, uint8_t* __restrict__ flags, int64_t* __restrict__ d_count,
     unsigned long long* __restrict__ ws, int64_t ntiles) {
   typedef CompactShape<T, D> S;
   constexpr int V = S::V, IT = S::IT, SUB = S::SUB, NSUB = S::NSUB, BT = S::BT, SLOT = S::SLOT, NBUF = S::NBUF;
   constexpr int PITCH = S::PITCH;
+  constexpr int kComputeWarps = S::kComputeWarps;
   constexpr int PER_WARP = NSUB / kComputeWarps;
   static_assert(NSUB % kComputeWarps == 0 && NSUB <= 32 && NBUF >= 2 && NBUF <= kTileRing - 2, "tile layout");
 
@@ -499,7 +500,7 @@ static cudaError_t launch_compact_variant(const T* in, int64_t ld_in, int64_t n,
   static int blocks_per_sm = 0;  // cached device attribute
   if (!blocks_per_sm) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, kThreads, smem);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, S::kThreads, smem);
     if (e != cudaSuccess || blocks_per_sm < 1) blocks_per_sm = 1;
   }
   // block 0 is the global scanner; the cooperative launch keeps every block resident, so
@@ -509,7 +510,7 @@ static cudaError_t launch_compact_variant(const T* in, int64_t ld_in, int64_t n,
   void* args[] = {(void*)&in,     (void*)&ld_in,     (void*)&n,          (void*)&w,     (void*)&out,
                   (void*)&ld_out, (void*)&out_index, (void*)&index_base, (void*)&flags, (void*)&d_count,
                   (void*)&ws,     (void*)&ntiles};
-  return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(kThreads), args, smem, s);
+  return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(S::kThreads), args, smem, s);
 }
 
 template <typename T, int D>

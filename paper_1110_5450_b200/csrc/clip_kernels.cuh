@@ -17,25 +17,37 @@ template <typename T> __host__ __device__ constexpr int vec_elems() { return 16 
 // Compacting kernel: a warp sub-tile is 32 lanes x 4 segments (fp64 lanes load two
 // 128-bit vectors); a block tile is compact_subtiles() sub-tiles; compact_buffers() block
 // tiles are staged in shared memory at once (the copy-out lags the compute by that many
-// minus one), sized to stay near 100 KB of shared memory per block.
+// minus one).
 template <typename T> __host__ __device__ constexpr int compact_items() { return 4 / vec_elems<T>(); }
-#ifndef CLIPSEG_NSUB_F32_2D  // tuning knobs of the headline (fp32, 2D) instantiation
-#define CLIPSEG_NSUB_F32_2D 16
+#ifndef CLIPSEG_COMPUTE_WARPS  // tuning knobs of the headline (fp32, 2D) instantiation
+#define CLIPSEG_COMPUTE_WARPS 16   // compute warps per block
+#endif
+#ifndef CLIPSEG_NSUB_F32_2D
+#define CLIPSEG_NSUB_F32_2D 32     // sub-tiles (of 128 segments) per block tile
 #endif
 #ifndef CLIPSEG_NBUF_F32_2D
-#define CLIPSEG_NBUF_F32_2D 3
+#define CLIPSEG_NBUF_F32_2D 3      // block tiles staged in shared memory at once
 #endif
 #ifndef CLIPSEG_MINB_F32_2D
-#define CLIPSEG_MINB_F32_2D 2
+#define CLIPSEG_MINB_F32_2D 1      // resident blocks per SM the register budget targets
 #endif
+// fp32 2D (the bench workload): one block per SM, 16 compute warps, 4096-segment tiles,
+// 3 staged (~203 KB); fp32 3D: 16 warps, 2048-segment tiles; fp64: 8 compute warps and
+// 1024-segment tiles, so the wider rows keep enough registers.
+template <typename T, int D> __host__ __device__ constexpr bool compact_headline() {
+  return sizeof(T) == 4 && D == 2;
+}
+template <typename T, int D> __host__ __device__ constexpr int compact_warps() {
+  return compact_headline<T, D>() ? CLIPSEG_COMPUTE_WARPS : (sizeof(T) == 4 ? 16 : 8);
+}
 template <typename T, int D> __host__ __device__ constexpr int compact_subtiles() {
-  return (sizeof(T) == 4 && D == 2) ? CLIPSEG_NSUB_F32_2D : 8;
+  return compact_headline<T, D>() ? CLIPSEG_NSUB_F32_2D : (sizeof(T) == 4 ? 16 : 8);
 }
 template <typename T, int D> __host__ __device__ constexpr int compact_buffers() {
-  return (sizeof(T) == 4 && D == 2) ? CLIPSEG_NBUF_F32_2D : ((sizeof(T) == 8 && D == 3) ? 2 : 3);
+  return compact_headline<T, D>() ? CLIPSEG_NBUF_F32_2D : ((sizeof(T) == 8 && D == 3) ? 2 : 3);
 }
 template <typename T, int D> __host__ __device__ constexpr int compact_min_blocks() {
-  return (sizeof(T) == 4 && D == 2) ? CLIPSEG_MINB_F32_2D : 1;
+  return compact_headline<T, D>() ? CLIPSEG_MINB_F32_2D : 1;
 }
 // Smallest block tile over all (T, D): the workspace is sized with it.
 constexpr int64_t kMinCompactTile = 8 * 128;
