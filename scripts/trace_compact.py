@@ -40,7 +40,7 @@ def main():
                b.flags.data_ptr(), b.count.data_ptr(), b.ws.data_ptr(), b.ws.numel(), s)
         assert st == 0
         torch.cuda.synchronize()
-    ntiles = (n + 2047) // 2048
+    ntiles = (n + int(os.environ.get("BT", "4096")) - 1) // int(os.environ.get("BT", "4096"))
     buf = np.zeros(min(ntiles, 1 << 19) * 8, dtype=np.uint64)
     assert L.clip_trace_read(buf.ctypes.data, buf.nbytes) == 0
     t = buf.reshape(-1, 8).astype(np.int64)
