@@ -28,7 +28,7 @@ CLIPSEG_SO = os.path.join(ROOT, "paper_1110_5450_b200", "lib", "libclipseg.so")
 
 SYNTH_SRC = [os.path.join(ROOT, "synth", f) for f in ("synth.cu", "synth_core.h")] + [
     os.path.join(ROOT, "include", "synth.h")]
-ORACLE_SRC = [os.path.join(ROOT, "oracle", f) for f in ("clip_oracle.c", "clip_oracle_impl.h")]
+ORACLE_SRC = [os.path.join(ROOT, "oracle", f) for f in ("clip_oracle.c", "clip_oracle_impl.h", "clip_homog_impl.h")]
 CSRC = os.path.join(ROOT, "paper_1110_5450_b200", "csrc")
 
 

@@ -33,6 +33,17 @@ def _trace_type(real):
 
 
 _TRACE = {np.float32: _trace_type(ctypes.c_float), np.float64: _trace_type(ctypes.c_double)}
+
+
+def _htrace_type(real):
+    class HTrace(ctypes.Structure):
+        _fields_ = [("c0", ctypes.c_uint), ("c1", ctypes.c_uint), ("visible", ctypes.c_int),
+                    ("t_in", real), ("t_out", real), ("a_in", real * 6), ("a_out", real * 6),
+                    ("has_in", ctypes.c_int * 6), ("has_out", ctypes.c_int * 6)]
+    return HTrace
+
+
+_HTRACE = {np.float32: _htrace_type(ctypes.c_float), np.float64: _htrace_type(ctypes.c_double)}
 _SFX = {np.float32: "f32", np.float64: "f64"}
 
 
@@ -53,6 +64,15 @@ def lib():
                 f.restype = ctypes.c_int64
                 f = getattr(L, "oracle_clip_one_" + s)
                 f.argtypes = [ctypes.c_int, _P, _P, _P, _P, _P]
+                f.restype = ctypes.c_int
+                f = getattr(L, "oracle_homog_clip_" + s)
+                f.argtypes = [_P, _I64, _I64, _P, _I64, _P, ctypes.c_int]
+                f.restype = ctypes.c_int
+                f = getattr(L, "oracle_homog_compact_" + s)
+                f.argtypes = [_P, _I64, _I64, _P, _I64, _P, _I64, _P, ctypes.c_int]
+                f.restype = ctypes.c_int64
+                f = getattr(L, "oracle_homog_one_" + s)
+                f.argtypes = [_P, _P, _P]
                 f.restype = ctypes.c_int
             _lib = L
     return _lib
@@ -129,6 +149,62 @@ def clip_one(p, lo, hi, dim, dtype=np.float32):
                  a_in=np.array(tr.a_in[:dim], dtype=dt), a_out=np.array(tr.a_out[:dim], dtype=dt),
                  has_in=list(tr.has_in[:dim]), has_out=list(tr.has_out[:dim]))
     return q[:2 * dim], bool(vis), trace
+
+
+# ---- NEXT-1: homogeneous clip space (oracle/clip_homog_impl.h, rules H1..H10) ----------
+# Input planes (8, ld): x0, y0, z0, w0, x1, y1, z1, w1.  Output: the same 8 homogeneous
+# planes, or with ndc=True the 6 divided ones x0/w0, y0/w0, z0/w0, x1/w1, y1/w1, z1/w1.
+
+def homog_clip(planes, n, ndc=False, nthreads=1):
+    """Dense homogeneous oracle: returns (out planes (8 or 6, ld), flags uint8[n])."""
+    dt = _dt(planes.dtype)
+    planes = np.ascontiguousarray(planes)
+    ld = planes.shape[1]
+    assert planes.shape[0] == 8 and n <= ld
+    out = np.empty((6 if ndc else 8, ld), dtype=dt)
+    flags = np.empty(n, dtype=np.uint8)
+    f = getattr(lib(), "oracle_homog_clip_" + _SFX[dt])
+    rows = planes.dtype.itemsize
+
+    def run(a, b):
+        st = f(planes.ctypes.data + a * rows, ld, b - a, out.ctypes.data + a * rows, ld, flags.ctypes.data + a,
+               int(ndc))
+        assert st == 0, st
+
+    _parallel(run, n, nthreads)
+    return out, flags
+
+
+def homog_compact(planes, n, index_base=0, with_flags=False, ndc=False):
+    """Compacting homogeneous oracle: (out (8 or 6, ld) first `count` rows valid, index, count[, flags])."""
+    dt = _dt(planes.dtype)
+    planes = np.ascontiguousarray(planes)
+    ld = planes.shape[1]
+    out = np.full((6 if ndc else 8, ld), np.nan, dtype=dt)
+    idx = np.empty(max(n, 1), dtype=np.int64)
+    flags = np.empty(max(n, 1), dtype=np.uint8)
+    f = getattr(lib(), "oracle_homog_compact_" + _SFX[dt])
+    cnt = f(_ptr(planes), ld, n, _ptr(out), ld, _ptr(idx), index_base, _ptr(flags), int(ndc))
+    assert cnt >= 0, cnt
+    if with_flags:
+        return out, idx[:cnt], int(cnt), flags[:n]
+    return out, idx[:cnt], int(cnt)
+
+
+def homog_one(p, dtype=np.float32):
+    """One segment p = (x0,y0,z0,w0,x1,y1,z1,w1); returns (q[8], visible, trace dict); the
+    trace's alphas are per plane j = 2k (w + x_k) / 2k + 1 (w - x_k)."""
+    dt = _dt(dtype)
+    pa = np.asarray(p, dtype=dt).copy()
+    assert pa.shape == (8,)
+    q = np.zeros(8, dtype=dt)
+    tr = _HTRACE[dt]()
+    vis = getattr(lib(), "oracle_homog_one_" + _SFX[dt])(_ptr(pa), _ptr(q), ctypes.addressof(tr))
+    assert vis in (0, 1)
+    trace = dict(c0=tr.c0, c1=tr.c1, visible=tr.visible, t_in=dt(tr.t_in), t_out=dt(tr.t_out),
+                 a_in=np.array(tr.a_in[:], dtype=dt), a_out=np.array(tr.a_out[:], dtype=dt),
+                 has_in=list(tr.has_in[:]), has_out=list(tr.has_out[:]))
+    return q, bool(vis), trace
 
 
 def _parallel(run, n, nthreads):

@@ -17,6 +17,10 @@
  * explicit fma of R7.  Pins: tests/test_oracle_*.py (worked examples, exact rational
  * reference, exact grid classifier, brute-force sampling, closed forms, invariants,
  * metamorphic relations, an independent iterative Cohen-Sutherland clipper).
+ *
+ * NEXT-1 (clip_homog_impl.h): the same procedure in homogeneous clip space, -w <= x, y, z
+ * <= w (Blinn & Newell's boundary coordinates), rules H1..H10; pinned by its reduction to
+ * the 3D cuboid rules at w = 1 and by tests/test_oracle_homog.py.
  */
 #include <math.h>
 #include <stdint.h>
@@ -38,6 +42,23 @@ typedef struct {
   int has_in[3], has_out[3];
 } oracle_trace_f64;
 
+/* NEXT-1 trace: six planes (j = 2k low, 2k + 1 high) */
+typedef struct {
+  unsigned c0, c1;
+  int visible;
+  float t_in, t_out;
+  float a_in[6], a_out[6];
+  int has_in[6], has_out[6];
+} oracle_htrace_f32;
+
+typedef struct {
+  unsigned c0, c1;
+  int visible;
+  double t_in, t_out;
+  double a_in[6], a_out[6];
+  int has_in[6], has_out[6];
+} oracle_htrace_f64;
+
 static int window_ok_(int dim) { return dim == 2 || dim == 3; }
 
 static float canonical_nan_f32(void) {
@@ -58,6 +79,7 @@ static double canonical_nan_f64(void) {
 #define SFX f32
 #define FMA fmaf
 #include "clip_oracle_impl.h"
+#include "clip_homog_impl.h"
 #undef REAL
 #undef SFX
 #undef FMA
@@ -66,6 +88,7 @@ static double canonical_nan_f64(void) {
 #define SFX f64
 #define FMA fma
 #include "clip_oracle_impl.h"
+#include "clip_homog_impl.h"
 #undef REAL
 #undef SFX
 #undef FMA

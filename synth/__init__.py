@@ -16,7 +16,9 @@ _SO = os.path.join(_HERE, "libsynth.so")
 _lib = None
 _lock = threading.Lock()
 
-UNIFORM, MIX, ADVERSARIAL = 0, 1, 2
+UNIFORM, MIX, ADVERSARIAL, HOMOG = 0, 1, 2, 3
+# HOMOG (dim 4: planes x0,y0,z0,w0,x1,y1,z1,w1) tags
+H_PERSPECTIVE, H_AFFINE, H_BEHIND, H_ON_PLANE, H_DEGENERATE = 0, 1, 2, 3, 4
 CAT_INSIDE, CAT_CROSSING, CAT_OUTSIDE = 0, 1, 2
 TAG_NEAR = 0x80
 

@@ -9,12 +9,19 @@
 
 namespace {
 
+// D == 4 is the homogeneous family (syn_homog); D = 2, 3 the cuboid families.
+template <typename T, int D>
+SYN_HD uint8_t gen_one(int family, uint64_t seed, int64_t i, uint32_t p_in, uint32_t p_cross, T (&p)[2 * D]) {
+  if constexpr (D == 4) return syn_homog<T>(seed, i, p);
+  else return syn_segment<T, D>(family, seed, i, p_in, p_cross, p);
+}
+
 template <typename T, int D>
 void fill_host_range(int family, uint64_t seed, int64_t i0, int64_t a, int64_t b, T* planes, int64_t ld,
                      uint8_t* tag, uint32_t p_in, uint32_t p_cross) {
   T p[2 * D];
   for (int64_t r = a; r < b; ++r) {
-    const uint8_t t = syn_segment<T, D>(family, seed, i0 + r, p_in, p_cross, p);
+    const uint8_t t = gen_one<T, D>(family, seed, i0 + r, p_in, p_cross, p);
     for (int c = 0; c < 2 * D; ++c) planes[(int64_t)c * ld + r] = p[c];
     if (tag) tag[r] = t;
   }
@@ -42,7 +49,7 @@ __global__ void fill_kernel(int family, uint64_t seed, int64_t i0, int64_t n, T*
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride) {
     T p[2 * D];
-    const uint8_t t = syn_segment<T, D>(family, seed, i0 + r, p_in, p_cross, p);
+    const uint8_t t = gen_one<T, D>(family, seed, i0 + r, p_in, p_cross, p);
 #pragma unroll
     for (int c = 0; c < 2 * D; ++c) planes[(int64_t)c * ld + r] = p[c];
     if (tag) tag[r] = t;
@@ -63,8 +70,8 @@ int fill_device(int family, uint64_t seed, int64_t i0, int64_t n, T* planes, int
 }
 
 int check(int family, int dim, int64_t i0, int64_t n, const void* planes, int64_t ld) {
-  if (family < SYN_UNIFORM || family > SYN_ADVERSARIAL) return SYNTH_EINVAL;
-  if (dim != 2 && dim != 3) return SYNTH_EINVAL;
+  if (family < SYN_UNIFORM || family > SYN_HOMOG) return SYNTH_EINVAL;
+  if (family == SYN_HOMOG ? dim != 4 : (dim != 2 && dim != 3)) return SYNTH_EINVAL;
   if (n < 0 || i0 < 0 || ld < n) return SYNTH_EINVAL;
   if (n > 0 && !planes) return SYNTH_EINVAL;
   return SYNTH_OK;
@@ -78,6 +85,7 @@ int synth_fill_host_f32(int family, int dim, uint64_t seed, int64_t i0, int64_t 
                         uint8_t* tag, uint32_t p_in, uint32_t p_cross, int nthreads) {
   const int s = check(family, dim, i0, n, planes, ld);
   if (s) return s;
+  if (dim == 4) return fill_host<float, 4>(family, seed, i0, n, planes, ld, tag, p_in, p_cross, nthreads);
   return dim == 2 ? fill_host<float, 2>(family, seed, i0, n, planes, ld, tag, p_in, p_cross, nthreads)
                   : fill_host<float, 3>(family, seed, i0, n, planes, ld, tag, p_in, p_cross, nthreads);
 }
@@ -86,6 +94,7 @@ int synth_fill_host_f64(int family, int dim, uint64_t seed, int64_t i0, int64_t 
                         uint8_t* tag, uint32_t p_in, uint32_t p_cross, int nthreads) {
   const int s = check(family, dim, i0, n, planes, ld);
   if (s) return s;
+  if (dim == 4) return fill_host<double, 4>(family, seed, i0, n, planes, ld, tag, p_in, p_cross, nthreads);
   return dim == 2 ? fill_host<double, 2>(family, seed, i0, n, planes, ld, tag, p_in, p_cross, nthreads)
                   : fill_host<double, 3>(family, seed, i0, n, planes, ld, tag, p_in, p_cross, nthreads);
 }
@@ -94,6 +103,7 @@ int synth_fill_device_f32(int family, int dim, uint64_t seed, int64_t i0, int64_
                           uint8_t* tag, uint32_t p_in, uint32_t p_cross, void* stream) {
   const int s = check(family, dim, i0, n, planes, ld);
   if (s) return s;
+  if (dim == 4) return fill_device<float, 4>(family, seed, i0, n, planes, ld, tag, p_in, p_cross, stream);
   return dim == 2 ? fill_device<float, 2>(family, seed, i0, n, planes, ld, tag, p_in, p_cross, stream)
                   : fill_device<float, 3>(family, seed, i0, n, planes, ld, tag, p_in, p_cross, stream);
 }
@@ -102,6 +112,7 @@ int synth_fill_device_f64(int family, int dim, uint64_t seed, int64_t i0, int64_
                           uint8_t* tag, uint32_t p_in, uint32_t p_cross, void* stream) {
   const int s = check(family, dim, i0, n, planes, ld);
   if (s) return s;
+  if (dim == 4) return fill_device<double, 4>(family, seed, i0, n, planes, ld, tag, p_in, p_cross, stream);
   return dim == 2 ? fill_device<double, 2>(family, seed, i0, n, planes, ld, tag, p_in, p_cross, stream)
                   : fill_device<double, 3>(family, seed, i0, n, planes, ld, tag, p_in, p_cross, stream);
 }

@@ -22,7 +22,9 @@
 #define SYN_HD static inline
 #endif
 
-enum { SYN_UNIFORM = 0, SYN_MIX = 1, SYN_ADVERSARIAL = 2 };
+enum { SYN_UNIFORM = 0, SYN_MIX = 1, SYN_ADVERSARIAL = 2, SYN_HOMOG = 3 };
+/* SYN_HOMOG (dim 4 only: x0,y0,z0,w0,x1,y1,z1,w1) tags */
+enum { SYN_H_PERSPECTIVE = 0, SYN_H_AFFINE = 1, SYN_H_BEHIND = 2, SYN_H_ON_PLANE = 3, SYN_H_DEGENERATE = 4 };
 enum { SYN_CAT_INSIDE = 0, SYN_CAT_CROSSING = 1, SYN_CAT_OUTSIDE = 2 };
 #define SYN_TAG_NEAR 0x80u  /* adversarial tag bit: endpoint placed within tolerance of an edge */
 
@@ -61,6 +63,8 @@ template <> struct SynT<float> {
     else b = (uint32_t)((int64_t)b + k);
     float r; memcpy(&r, &b, 4); return r;
   }
+  /* positive w in [0.5, 2): (3k + 2^22) * 2^-23, k < 2^22 (exact) */
+  SYN_HD static float wpos(uint64_t h) { return (float)(3u * (uint32_t)(h & 0x3FFFFFull) + 0x400000u) * 0x1p-23f; }
   SYN_HD static float min_sub() { return 0x1p-149f; }
   SYN_HD static float neg_zero() { uint32_t b = 0x80000000u; float r; memcpy(&r, &b, 4); return r; }
 };
@@ -82,6 +86,7 @@ template <> struct SynT<double> {
     else b = (uint64_t)((int64_t)b + k);
     double r; memcpy(&r, &b, 8); return r;
   }
+  SYN_HD static double wpos(uint64_t h) { return (double)(3ull * (h >> 14) + (1ull << 50)) * 0x1p-51; }
   SYN_HD static double min_sub() { return 0x1p-1074; }
   SYN_HD static double neg_zero() { uint64_t b = 0x8000000000000000ull; double r; memcpy(&r, &b, 8); return r; }
 };
@@ -244,4 +249,44 @@ SYN_HD uint8_t syn_segment(int family, uint64_t seed, int64_t i, uint32_t p_in, 
       break;
   }
   return tag;
+}
+
+/* NEXT-1 input: one segment in homogeneous clip space, p = (x0,y0,z0,w0,x1,y1,z1,w1), around
+ * the volume -w <= x,y,z <= w.  Mode (tag) from the segment's draw 15:
+ *   60 % perspective: w in [0.5, 2), x,y,z = 2 g - 1 in [-3, 3) (g on the grid);
+ *   10 % affine: w = 1 exactly (the 3D cuboid reduction), x,y,z as above;
+ *   10 % behind: one endpoint with w in (-2, -0.5];
+ *   10 % on planes: one endpoint exactly on a plane (x = +-w) or an edge/corner of the volume;
+ *   10 % degenerate: an endpoint with w = 0 (the 4D origin, or a random direction), or a
+ *        zero-length segment. */
+template <typename T>
+SYN_HD uint8_t syn_homog(uint64_t seed, int64_t i, T p[8]) {
+  typedef SynT<T> S;
+  const uint64_t h0 = syn_h(seed, i, 15);
+  const int m = (int)((h0 >> 32) % 10u);
+  for (int e = 0; e < 2; ++e) {
+    for (int k = 0; k < 3; ++k) p[4 * e + k] = (T)2 * S::grid(syn_h(seed, i, 4 * e + k)) - (T)1;
+    p[4 * e + 3] = (m == 6) ? (T)1 : S::wpos(syn_h(seed, i, 4 * e + 3));
+  }
+  const int e = (int)(h0 & 1u);
+  T* P = p + 4 * e;
+  if (m < 6) return SYN_H_PERSPECTIVE;
+  if (m == 6) return SYN_H_AFFINE;
+  if (m == 7) {
+    P[3] = -P[3];
+    return SYN_H_BEHIND;
+  }
+  if (m == 8) {
+    const int a = (int)((h0 >> 1) % 3u), nb = (int)((h0 >> 3) & 3u);  /* axis, extra planes */
+    for (int j = 0; j <= (nb == 3 ? 2 : nb); ++j) {
+      const int ax = (a + j) % 3;
+      P[ax] = ((h0 >> (5 + j)) & 1u) ? P[3] : -P[3];
+    }
+    return SYN_H_ON_PLANE;
+  }
+  const int s = (int)((h0 >> 1) & 3u);
+  if (s == 0) { P[0] = P[1] = P[2] = P[3] = (T)0; }                      /* the 4D origin */
+  else if (s == 1) { P[3] = (T)0; }                                       /* w = 0 direction */
+  else { for (int k = 0; k < 4; ++k) p[4 * (1 - e) + k] = P[k]; }         /* zero length */
+  return SYN_H_DEGENERATE;
 }

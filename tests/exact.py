@@ -124,3 +124,28 @@ def classic_cohen_sutherland(p0, p1, lo, hi):
         else:
             x1, y1 = x, y; c1 = code(x1, y1)
     return False, None
+
+
+def exact_homog_clip(p0, p1):
+    """Exact clip of the homogeneous segment P0P1 (x, y, z, w) against the closed volume
+    -w <= x, y, z <= w (Blinn & Newell), by the parametric (Liang–Barsky) method in exact
+    rationals: each plane's boundary coordinate B(t) = B0 + t (B1 - B0) must stay >= 0.
+    Returns (Q0, Q1, t_in, t_out) as Fractions (4 components each), or None."""
+    P0 = [Fraction(x) for x in p0]
+    P1 = [Fraction(x) for x in p1]
+    t_in, t_out = Fraction(0), Fraction(1)
+    for k in range(3):
+        for s in (1, -1):  # w + x_k >= 0 and w - x_k >= 0
+            b0 = P0[3] + s * P0[k]
+            b1 = P1[3] + s * P1[k]
+            if b0 < 0 and b1 < 0:
+                return None
+            if b0 < 0 <= b1:
+                t_in = max(t_in, b0 / (b0 - b1))
+            elif b1 < 0 <= b0:
+                t_out = min(t_out, b0 / (b0 - b1))
+    if t_in > t_out:
+        return None
+    Q0 = [P0[c] + t_in * (P1[c] - P0[c]) for c in range(4)]
+    Q1 = [P0[c] + t_out * (P1[c] - P0[c]) for c in range(4)]
+    return Q0, Q1, t_in, t_out

@@ -64,3 +64,33 @@ def test_bad_arguments():
         synth.fill_host(5, 2, 1, 10)
     with pytest.raises(ValueError):
         synth.fill_host(0, 4, 1, 10)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_homog_recipe(dtype):
+    """NEXT-1 inputs (dim 4): shard invariance, exact grid values, every mode as built."""
+    full, tf = synth.fill_host(synth.HOMOG, 4, 91, 60000, dtype=dtype, nthreads=4)
+    part, tp = synth.fill_host(synth.HOMOG, 4, 91, 777, dtype=dtype, i0=5000, nthreads=1)
+    assert np.array_equal(full[:, 5000:5777].view(np.uint8), part[:, :777].view(np.uint8))
+    assert np.array_equal(tf[5000:5777], tp)
+    n = 60000
+    p = full[:, :n].astype(np.float64)
+    frac = np.bincount(tf, minlength=5) / n
+    assert abs(frac[0] - 0.6) < 0.02 and np.all(np.abs(frac[1:] - 0.1) < 0.01)
+    pers = tf == synth.H_PERSPECTIVE
+    for e in range(2):
+        w = p[4 * e + 3, pers]
+        assert w.min() >= 0.5 and w.max() < 2
+        assert np.abs(p[4 * e:4 * e + 3, pers]).max() <= 3
+    aff = tf == synth.H_AFFINE
+    assert np.all(p[[3, 7]][:, aff] == 1)
+    beh = tf == synth.H_BEHIND
+    assert np.all((p[3, beh] < 0) ^ (p[7, beh] < 0))
+    onp = tf == synth.H_ON_PLANE
+    on_any = np.zeros(onp.sum(), bool)
+    for e in range(2):
+        on_any |= np.any(np.abs(p[4 * e:4 * e + 3, onp]) == p[4 * e + 3, onp], axis=0)
+    assert on_any.all()
+    scale = 2**21 if dtype == np.float32 else 2**49
+    xyz = p[[0, 1, 2, 4, 5, 6]][:, pers] * scale
+    assert np.array_equal(xyz, np.rint(xyz))                        # x, y, z on the grid (exact)
