@@ -114,6 +114,31 @@ int clip_segments_compact_host_f64(const double* h_in, int64_t ld_in, int64_t n,
                                    double* h_out, int64_t ld_out, uint8_t* h_flags, int64_t* h_count,
                                    int64_t chunk, void* d_staging, size_t staging_bytes);
 
+/* ---- NEXT-1: segments in homogeneous clip space (rules H1-H10) --------
+ * The clip volume is the closed -w <= x, y, z <= w (Blinn & Newell; the textbook home of
+ * the window-edge coordinates \wec / \WEC that PAPER.md:29-30 names).
+ * in:    8 planes (ld_in): x0, y0, z0, w0, x1, y1, z1, w1.
+ * ndc:   0 -> out has 8 planes: the clipped homogeneous endpoints (copied when inside,
+ *             interpolated with the crossed plane snapped to -q_w / q_w and the other axes
+ *             clamped into [-q_w, q_w] otherwise);
+ *        1 -> out has 6 planes: the perspective-divided endpoints q_k / q_w (qNaN for an
+ *             endpoint with q_w = 0, i.e. at the 4D origin).
+ *        anything else -> CLIP_EINVAL.
+ * Otherwise as the cuboid calls above: dense rows of invisible segments are canonical qNaN,
+ * flags (nullable) 1/0, the compacting call keeps visible rows in input order with optional
+ * global indices and a device count, workspace clip_compact_workspace_bytes(n), out must not
+ * overlap in (compacting call), same status codes and alignment rules. */
+int clip_homog_segments_f32(const float* in, int64_t ld_in, int64_t n, int ndc, float* out, int64_t ld_out,
+                            uint8_t* flags, void* stream);
+int clip_homog_segments_f64(const double* in, int64_t ld_in, int64_t n, int ndc, double* out, int64_t ld_out,
+                            uint8_t* flags, void* stream);
+int clip_homog_segments_compact_f32(const float* in, int64_t ld_in, int64_t n, int ndc, float* out,
+                                    int64_t ld_out, int64_t* out_index, int64_t index_base, uint8_t* flags,
+                                    int64_t* d_count, void* workspace, size_t workspace_bytes, void* stream);
+int clip_homog_segments_compact_f64(const double* in, int64_t ld_in, int64_t n, int ndc, double* out,
+                                    int64_t ld_out, int64_t* out_index, int64_t index_base, uint8_t* flags,
+                                    int64_t* d_count, void* workspace, size_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

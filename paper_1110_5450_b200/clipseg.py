@@ -46,6 +46,12 @@ def _load():
         f = getattr(L, "clip_segments_compact_host_" + s)
         f.argtypes = [P, I64, I64, ctypes.POINTER(W), P, I64, U8P, ctypes.POINTER(I64), I64, P, SZ]
         f.restype = ctypes.c_int
+        f = getattr(L, "clip_homog_segments_" + s)
+        f.argtypes = [P, I64, I64, ctypes.c_int, P, I64, U8P, P]
+        f.restype = ctypes.c_int
+        f = getattr(L, "clip_homog_segments_compact_" + s)
+        f.argtypes = [P, I64, I64, ctypes.c_int, P, I64, P, I64, U8P, P, P, SZ, P]
+        f.restype = ctypes.c_int
     L.clip_compact_workspace_bytes.argtypes = [I64]
     L.clip_compact_workspace_bytes.restype = SZ
     L.clip_host_staging_bytes.argtypes = [ctypes.c_int, ctypes.c_int, I64]
@@ -69,11 +75,16 @@ clip_shard_offsets = _lib.clip_shard_offsets
 clip_host_staging_bytes = _lib.clip_host_staging_bytes
 clip_segments_compact_host_f32 = _lib.clip_segments_compact_host_f32
 clip_segments_compact_host_f64 = _lib.clip_segments_compact_host_f64
+clip_homog_segments_f32 = _lib.clip_homog_segments_f32
+clip_homog_segments_f64 = _lib.clip_homog_segments_f64
+clip_homog_segments_compact_f32 = _lib.clip_homog_segments_compact_f32
+clip_homog_segments_compact_f64 = _lib.clip_homog_segments_compact_f64
 
 EXPORTED = ["clip_plane_stride", "clip_status_string", "clip_segments_f32", "clip_segments_f64",
             "clip_compact_workspace_bytes", "clip_segments_compact_f32", "clip_segments_compact_f64",
             "clip_shard_offsets", "clip_host_staging_bytes", "clip_segments_compact_host_f32",
-            "clip_segments_compact_host_f64"]
+            "clip_segments_compact_host_f64", "clip_homog_segments_f32", "clip_homog_segments_f64",
+            "clip_homog_segments_compact_f32", "clip_homog_segments_compact_f64"]
 
 
 class ClipError(RuntimeError):
@@ -198,6 +209,46 @@ def clip_compact_host(h_planes, n, lo, hi, h_out, h_flags=None, chunk=1 << 24, s
     _check(f(pin, ld_in, n, ctypes.byref(w), pout, ld_out, fl, ctypes.byref(cnt), chunk, staging.data_ptr(),
              staging.numel()), "clip_segments_compact_host")
     return cnt.value, staging
+
+
+# ---- NEXT-1: homogeneous clip space (planes x0, y0, z0, w0, x1, y1, z1, w1) --------------
+def clip_homog(planes, n, ndc=False, out=None, flags=None, want_flags=True, stream=None):
+    """Dense homogeneous clip of n segments in `planes` (8, ld) -> (out (8 or 6 with ndc, ld), flags)."""
+    torch = _torch()
+    assert planes.shape[0] == 8
+    sfx = _sfx(planes)
+    if out is None:
+        out = torch.empty((6 if ndc else 8, planes.shape[1]), dtype=planes.dtype, device=planes.device)
+    if flags is None and want_flags:
+        flags = torch.empty(max(n, 1), dtype=torch.uint8, device=planes.device)
+    f = clip_homog_segments_f32 if sfx == "f32" else clip_homog_segments_f64
+    _check(f(planes.data_ptr(), planes.stride(0), n, int(ndc), out.data_ptr(), out.stride(0),
+             flags.data_ptr() if flags is not None else None, _stream(stream)), "clip_homog_segments_" + sfx)
+    return out, flags
+
+
+class HomogBuffers(CompactBuffers):
+    """Reusable outputs + workspace for the compacting homogeneous clip (8 or 6 output planes)."""
+
+    def __init__(self, n, dtype, ndc=False, device="cuda", with_index=False, with_flags=False):
+        torch = _torch()
+        super().__init__(n, 3, dtype, device, with_index, with_flags)
+        self.ndc = ndc
+        self.out = torch.empty((6 if ndc else 8, clip_plane_stride(n)), dtype=dtype, device=device)
+
+
+def clip_homog_compact(planes, n, ndc=False, bufs: HomogBuffers | None = None, with_index=False,
+                       with_flags=False, index_base=0, stream=None):
+    """Stable compacting homogeneous clip -> HomogBuffers (out rows [0, count) valid)."""
+    sfx = _sfx(planes)
+    if bufs is None:
+        bufs = HomogBuffers(n, planes.dtype, ndc, planes.device, with_index, with_flags)
+    f = clip_homog_segments_compact_f32 if sfx == "f32" else clip_homog_segments_compact_f64
+    _check(f(planes.data_ptr(), planes.stride(0), n, int(ndc), bufs.out.data_ptr(), bufs.out.stride(0),
+             bufs.index.data_ptr() if bufs.index is not None else None, index_base,
+             bufs.flags.data_ptr() if bufs.flags is not None else None, bufs.count.data_ptr(),
+             bufs.ws.data_ptr(), bufs.ws.numel(), _stream(stream)), "clip_homog_segments_compact_" + sfx)
+    return bufs
 
 
 def shard_offsets(counts_t, rank, stream=None):

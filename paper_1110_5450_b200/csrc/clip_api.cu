@@ -64,8 +64,9 @@ int dense(const T* in, int64_t ld_in, int64_t n, const typename WinT<T>::type* w
   if ((st = check_planes(in, ld_in, n)) || (st = check_planes(out, ld_out, n))) return st;
   if (flags && !aligned(flags, 4)) return CLIP_EALIGN;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (win->dim == 2) return status_of(launch_dense<T, 2>(in, ld_in, n, to_window<T, 2>(win), out, ld_out, flags, s));
-  return status_of(launch_dense<T, 3>(in, ld_in, n, to_window<T, 3>(win), out, ld_out, flags, s));
+  if (win->dim == 2)
+    return status_of(launch_dense<T, BoxOp<T, 2>>(in, ld_in, n, to_window<T, 2>(win), out, ld_out, flags, s));
+  return status_of(launch_dense<T, BoxOp<T, 3>>(in, ld_in, n, to_window<T, 3>(win), out, ld_out, flags, s));
 }
 
 template <typename T>
@@ -91,10 +92,51 @@ int compact(const T* in, int64_t ld_in, int64_t n, const typename WinT<T>::type*
   const int64_t obytes = ((int64_t)(2 * dim - 1) * ld_out + n) * (int64_t)sizeof(T);
   if (ob < ib + ibytes && ib < ob + obytes) return CLIP_EINVAL;
   if (dim == 2)
-    return status_of(launch_compact<T, 2>(in, ld_in, n, to_window<T, 2>(win), out, ld_out, out_index, index_base,
-                                          flags, d_count, ws, s));
-  return status_of(launch_compact<T, 3>(in, ld_in, n, to_window<T, 3>(win), out, ld_out, out_index, index_base, flags,
-                                        d_count, ws, s));
+    return status_of(launch_compact<T, BoxOp<T, 2>>(in, ld_in, n, to_window<T, 2>(win), out, ld_out, out_index,
+                                                    index_base, flags, d_count, ws, s));
+  return status_of(launch_compact<T, BoxOp<T, 3>>(in, ld_in, n, to_window<T, 3>(win), out, ld_out, out_index,
+                                                  index_base, flags, d_count, ws, s));
+}
+
+// ---- NEXT-1: homogeneous clip space (8 input planes; 8 output planes, or 6 with ndc) ----
+template <typename T>
+int homog_dense(const T* in, int64_t ld_in, int64_t n, int ndc, T* out, int64_t ld_out, uint8_t* flags,
+                void* stream) {
+  if (n < 0 || (ndc != 0 && ndc != 1)) return CLIP_EINVAL;
+  if (n == 0) return CLIP_OK;
+  int st;
+  if ((st = check_planes(in, ld_in, n)) || (st = check_planes(out, ld_out, n))) return st;
+  if (flags && !aligned(flags, 4)) return CLIP_EALIGN;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const NoParams none{0};
+  if (ndc) return status_of(launch_dense<T, HomogOp<T, true>>(in, ld_in, n, none, out, ld_out, flags, s));
+  return status_of(launch_dense<T, HomogOp<T, false>>(in, ld_in, n, none, out, ld_out, flags, s));
+}
+
+template <typename T>
+int homog_compact(const T* in, int64_t ld_in, int64_t n, int ndc, T* out, int64_t ld_out, int64_t* out_index,
+                  int64_t index_base, uint8_t* flags, int64_t* d_count, void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || !d_count || (ndc != 0 && ndc != 1)) return CLIP_EINVAL;
+  if (!aligned(d_count, 8)) return CLIP_EALIGN;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (n == 0) return status_of(cudaMemsetAsync(d_count, 0, sizeof(int64_t), s));
+  int st;
+  if ((st = check_planes(in, ld_in, n)) || (st = check_planes(out, ld_out, n))) return st;
+  if (flags && !aligned(flags, 4)) return CLIP_EALIGN;
+  if (out_index && !aligned(out_index, 8)) return CLIP_EALIGN;
+  if (!ws) return CLIP_EINVAL;
+  if (!aligned(ws, 16)) return CLIP_EALIGN;
+  if (ws_bytes < clip_compact_workspace_bytes(n)) return CLIP_ENOSPACE;
+  const char *ib = reinterpret_cast<const char*>(in), *ob = reinterpret_cast<const char*>(out);
+  const int64_t ibytes = ((int64_t)7 * ld_in + n) * (int64_t)sizeof(T);
+  const int64_t obytes = ((int64_t)(ndc ? 5 : 7) * ld_out + n) * (int64_t)sizeof(T);
+  if (ob < ib + ibytes && ib < ob + obytes) return CLIP_EINVAL;
+  const NoParams none{0};
+  if (ndc)
+    return status_of(launch_compact<T, HomogOp<T, true>>(in, ld_in, n, none, out, ld_out, out_index, index_base,
+                                                         flags, d_count, ws, s));
+  return status_of(launch_compact<T, HomogOp<T, false>>(in, ld_in, n, none, out, ld_out, out_index, index_base,
+                                                        flags, d_count, ws, s));
 }
 
 // ---- pipelined host-buffer path -----------------------------------------------------
@@ -285,6 +327,30 @@ int clip_segments_compact_host_f64(const double* h_in, int64_t ld_in, int64_t n,
                                    double* h_out, int64_t ld_out, uint8_t* h_flags, int64_t* h_count, int64_t chunk,
                                    void* d_staging, size_t staging_bytes) {
   return compact_host<double>(h_in, ld_in, n, win, h_out, ld_out, h_flags, h_count, chunk, d_staging, staging_bytes);
+}
+
+int clip_homog_segments_f32(const float* in, int64_t ld_in, int64_t n, int ndc, float* out, int64_t ld_out,
+                            uint8_t* flags, void* stream) {
+  return homog_dense<float>(in, ld_in, n, ndc, out, ld_out, flags, stream);
+}
+
+int clip_homog_segments_f64(const double* in, int64_t ld_in, int64_t n, int ndc, double* out, int64_t ld_out,
+                            uint8_t* flags, void* stream) {
+  return homog_dense<double>(in, ld_in, n, ndc, out, ld_out, flags, stream);
+}
+
+int clip_homog_segments_compact_f32(const float* in, int64_t ld_in, int64_t n, int ndc, float* out, int64_t ld_out,
+                                    int64_t* out_index, int64_t index_base, uint8_t* flags, int64_t* d_count,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+  return homog_compact<float>(in, ld_in, n, ndc, out, ld_out, out_index, index_base, flags, d_count, workspace,
+                              workspace_bytes, stream);
+}
+
+int clip_homog_segments_compact_f64(const double* in, int64_t ld_in, int64_t n, int ndc, double* out, int64_t ld_out,
+                                    int64_t* out_index, int64_t index_base, uint8_t* flags, int64_t* d_count,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+  return homog_compact<double>(in, ld_in, n, ndc, out, ld_out, out_index, index_base, flags, d_count, workspace,
+                               workspace_bytes, stream);
 }
 
 }  // extern "C"

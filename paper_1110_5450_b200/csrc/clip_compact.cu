@@ -170,28 +170,29 @@ __device__ __noinline__ void global_scanner(unsigned long long* status, int64_t 
 
 }  // namespace
 
-template <typename T, int D> struct CompactShape {
+template <typename T, class Op> struct CompactShape {
   static constexpr int V = Vec16<T>::N;                 // segments per 128-bit vector
   static constexpr int IT = compact_items<T>();          // vectors per lane per sub-tile
   static constexpr int SUB = 32 * V * IT;                // 128 segments per sub-tile
-  static constexpr int NSUB = compact_subtiles<T, D>();  // sub-tiles per block tile
+  static constexpr int NSUB = compact_subtiles<T, Op>();  // sub-tiles per block tile
   static constexpr int BT = NSUB * SUB;
-  static constexpr int NBUF = compact_buffers<T, D>();   // staged tiles in flight per block
+  static constexpr int NBUF = compact_buffers<T, Op>();   // staged tiles in flight per block
   static constexpr int PITCH = SUB + V;                  // staged plane pitch: rows + scratch row
-  static constexpr int SLOT = 2 * D * PITCH;             // staged elements per sub-tile
+  static constexpr int SLOT = Op::OUT * PITCH;           // staged elements per sub-tile
   static constexpr size_t kStageBytes = (size_t)NBUF * NSUB * SLOT * sizeof(T);
   static constexpr size_t kSmemBytes = kStageBytes + (size_t)NBUF * NSUB * (SUB + 1);  // + local indices
-  static constexpr int kMinBlocks = compact_min_blocks<T, D>();
-  static constexpr int kComputeWarps = compact_warps<T, D>();
+  static constexpr int kMinBlocks = compact_min_blocks<T, Op>();
+  static constexpr int kComputeWarps = compact_warps<T, Op>();
   static constexpr int kThreads = (kComputeWarps + 1) * 32;  // + the scan warp
 };
 
-template <typename T, int D, bool FLAGS, bool INDEX>
-__global__ void __launch_bounds__(CompactShape<T, D>::kThreads, CompactShape<T, D>::kMinBlocks) clip_compact_kernel(
-    const T* __restrict__ in, int64_t ld_in, int64_t n, Window<T, D> w, T* __restrict__ out, int64_t ld_out,
+template <typename T, class Op, bool FLAGS, bool INDEX>
+__global__ void __launch_bounds__(CompactShape<T, Op>::kThreads, CompactShape<T, Op>::kMinBlocks) clip_compact_kernel(
+    const T* __restrict__ in, int64_t ld_in, int64_t n, typename Op::Params w, T* __restrict__ out, int64_t ld_out,
     int64_t* __restrict__ out_index, int64_t index_base, uint8_t* __restrict__ flags, int64_t* __restrict__ d_count,
     unsigned long long* __restrict__ ws, int64_t ntiles) {
-  typedef CompactShape<T, D> S;
+  typedef CompactShape<T, Op> S;
+  constexpr int IN = Op::IN, OUT = Op::OUT;
   constexpr int V = S::V, IT = S::IT, SUB = S::SUB, NSUB = S::NSUB, BT = S::BT, SLOT = S::SLOT, NBUF = S::NBUF;
   constexpr int PITCH = S::PITCH;
   constexpr int kComputeWarps = S::kComputeWarps;
@@ -289,7 +290,7 @@ __global__ void __launch_bounds__(CompactShape<T, D>::kThreads, CompactShape<T, 
     const int64_t r = n - (t * BT + (int64_t)sub * SUB);
     return r >= SUB ? SUB : (r > 0 ? (int)r : 0);
   };
-  auto load = [&](int64_t t, int sub, T (&dst)[IT][2 * D][V], const bool FULL) {
+  auto load = [&](int64_t t, int sub, T (&dst)[IT][IN][V], const bool FULL) {
     const T* src = in + t * BT + (int64_t)sub * SUB;
     const int rem = FULL ? SUB : remaining(t, sub);
 #pragma unroll
@@ -297,10 +298,10 @@ __global__ void __launch_bounds__(CompactShape<T, D>::kThreads, CompactShape<T, 
       const int o = (32 * j + lane) * V;
       if (FULL || o < rem) {
 #pragma unroll
-        for (int c = 0; c < 2 * D; ++c) load_vec<T>(src + c * ld_in + o, dst[j][c]);
+        for (int c = 0; c < IN; ++c) load_vec<T>(src + c * ld_in + o, dst[j][c]);
       } else {
 #pragma unroll
-        for (int c = 0; c < 2 * D; ++c)
+        for (int c = 0; c < IN; ++c)
 #pragma unroll
           for (int v = 0; v < V; ++v) dst[j][c][v] = T(0);
       }
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(CompactShape<T, D>::kThreads, CompactShape<T, 
   };
   // Sub-tile loads run one ahead of the clipping, across tile boundaries: the next tile is
   // claimed as this one starts, and its first sub-tile is loaded during this one's last.
-  T buf[2][IT][2 * D][V];
+  T buf[2][IT][IN][V];
   mbar_wait(&mb_tile[0], 0u);
   int64_t tile = s_tile[0];
   if (tile < ntiles) load(tile, warp, buf[0], false);
@@ -339,16 +340,16 @@ __global__ void __launch_bounds__(CompactShape<T, D>::kThreads, CompactShape<T, 
           // sub-tile is copied out of buf[0] first.
           constexpr bool PING = (PER_WARP % 2) == 0;
           const int cur = PING ? (r & 1) : 0;
-          T held[IT][2 * D][V];
+          T held[IT][IN][V];
           if (!PING) {
 #pragma unroll
             for (int j = 0; j < IT; ++j)
 #pragma unroll
-              for (int c = 0; c < 2 * D; ++c)
+              for (int c = 0; c < IN; ++c)
 #pragma unroll
                 for (int v = 0; v < V; ++v) held[j][c][v] = buf[0][j][c][v];
           }
-          T (&dst)[IT][2 * D][V] = PING ? buf[cur ^ 1] : buf[0];
+          T (&dst)[IT][IN][V] = PING ? buf[cur ^ 1] : buf[0];
           if (r + 1 < PER_WARP) {
             load(tile, sub + kComputeWarps, dst, FULL);
           } else {
@@ -356,15 +357,15 @@ __global__ void __launch_bounds__(CompactShape<T, D>::kThreads, CompactShape<T, 
             next = s_tile[(k + 1) & kRingMask];
             if (next < ntiles) load(next, warp, dst, false);
           }
-          const T (&plane)[IT][2 * D][V] = PING ? buf[cur] : held;
+          const T (&plane)[IT][IN][V] = PING ? buf[cur] : held;
           const int rem = FULL ? SUB : remaining(tile, sub);
           uint8_t* fl = FLAGS ? flags + tile * BT + (int64_t)sub * SUB : nullptr;
-          T res[IT][2 * D][V];
+          T res[IT][OUT][V];
           unsigned vis[IT];
 #pragma unroll
           for (int j = 0; j < IT; ++j) {
             const int o = (32 * j + lane) * V;
-            vis[j] = clip_group<T, D, V, false>(plane[j], w, res[j]);
+            vis[j] = Op::template group<V, false>(plane[j], w, res[j]);
             if (!FULL) vis[j] &= (o >= rem) ? 0u : (o + V <= rem ? (1u << V) - 1u : (1u << (rem - o)) - 1u);
             if (FLAGS) {
               uint32_t packed = 0;
@@ -403,7 +404,7 @@ __global__ void __launch_bounds__(CompactShape<T, D>::kThreads, CompactShape<T, 
               const bool on = (vis[j] >> v) & 1u;
               T* row = st + (on ? pos : SUB);
 #pragma unroll
-              for (int c = 0; c < 2 * D; ++c) row[c * PITCH] = res[j][c][v];
+              for (int c = 0; c < OUT; ++c) row[c * PITCH] = res[j][c][v];
               if (INDEX) lix[sub * (SUB + 1) + (on ? pos : SUB)] = (uint8_t)((32 * j + lane) * V + v);
               pos += on;
             }
@@ -452,7 +453,7 @@ __global__ void __launch_bounds__(CompactShape<T, D>::kThreads, CompactShape<T, 
         const int64_t g0 = prefix + s_pre[pb][sub];
         const T* st = stg + sub * SLOT;
 #pragma unroll
-        for (int c = 0; c < 2 * D; ++c) {
+        for (int c = 0; c < OUT; ++c) {
           T* dst = out + c * ld_out + g0 + lane;
           const T* src = st + c * PITCH + lane;
 #pragma unroll
@@ -490,13 +491,13 @@ __global__ void __launch_bounds__(CompactShape<T, D>::kThreads, CompactShape<T, 
   }
 }
 
-template <typename T, int D, bool FLAGS, bool INDEX>
-static cudaError_t launch_compact_variant(const T* in, int64_t ld_in, int64_t n, const Window<T, D>& w, T* out,
+template <typename T, class Op, bool FLAGS, bool INDEX>
+static cudaError_t launch_compact_variant(const T* in, int64_t ld_in, int64_t n, const typename Op::Params& w, T* out,
                                          int64_t ld_out, int64_t* out_index, int64_t index_base, uint8_t* flags,
                                          int64_t* d_count, unsigned long long* ws, int64_t ntiles, cudaStream_t s) {
-  typedef CompactShape<T, D> S;
+  typedef CompactShape<T, Op> S;
   const size_t smem = S::kSmemBytes;
-  auto kern = clip_compact_kernel<T, D, FLAGS, INDEX>;
+  auto kern = clip_compact_kernel<T, Op, FLAGS, INDEX>;
   static int blocks_per_sm = 0;  // cached device attribute
   if (!blocks_per_sm) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -513,11 +514,11 @@ static cudaError_t launch_compact_variant(const T* in, int64_t ld_in, int64_t n,
   return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(S::kThreads), args, smem, s);
 }
 
-template <typename T, int D>
-cudaError_t launch_compact(const T* in, int64_t ld_in, int64_t n, const Window<T, D>& w, T* out, int64_t ld_out,
-                           int64_t* out_index, int64_t index_base, uint8_t* flags, int64_t* d_count, void* ws,
-                           cudaStream_t s) {
-  typedef CompactShape<T, D> S;
+template <typename T, class Op>
+cudaError_t launch_compact(const T* in, int64_t ld_in, int64_t n, const typename Op::Params& w, T* out,
+                           int64_t ld_out, int64_t* out_index, int64_t index_base, uint8_t* flags, int64_t* d_count,
+                           void* ws, cudaStream_t s) {
+  typedef CompactShape<T, Op> S;
   const int64_t ntiles = (n + S::BT - 1) / S::BT;
   cudaError_t e = cudaMemsetAsync(ws, 0, kWsHeaderBytes + (size_t)ntiles * 8, s);
   if (e != cudaSuccess) return e;
@@ -525,15 +526,15 @@ cudaError_t launch_compact(const T* in, int64_t ld_in, int64_t n, const Window<T
   // flags / out_index are optional outputs: one instantiation per combination, so the
   // per-segment code carries no test for them
   if (flags && out_index)
-    return launch_compact_variant<T, D, true, true>(in, ld_in, n, w, out, ld_out, out_index, index_base, flags,
+    return launch_compact_variant<T, Op, true, true>(in, ld_in, n, w, out, ld_out, out_index, index_base, flags,
                                                     d_count, wsp, ntiles, s);
   if (flags)
-    return launch_compact_variant<T, D, true, false>(in, ld_in, n, w, out, ld_out, out_index, index_base, flags,
+    return launch_compact_variant<T, Op, true, false>(in, ld_in, n, w, out, ld_out, out_index, index_base, flags,
                                                      d_count, wsp, ntiles, s);
   if (out_index)
-    return launch_compact_variant<T, D, false, true>(in, ld_in, n, w, out, ld_out, out_index, index_base, flags,
+    return launch_compact_variant<T, Op, false, true>(in, ld_in, n, w, out, ld_out, out_index, index_base, flags,
                                                      d_count, wsp, ntiles, s);
-  return launch_compact_variant<T, D, false, false>(in, ld_in, n, w, out, ld_out, out_index, index_base, flags,
+  return launch_compact_variant<T, Op, false, false>(in, ld_in, n, w, out, ld_out, out_index, index_base, flags,
                                                     d_count, wsp, ntiles, s);
 }
 
@@ -548,13 +549,25 @@ extern "C" int clip_trace_clear() {
 }
 #endif
 
-#define INST(T, D)                                                                                              \
-  template cudaError_t launch_compact<T, D>(const T*, int64_t, int64_t, const Window<T, D>&, T*, int64_t,      \
-                                            int64_t*, int64_t, uint8_t*, int64_t*, void*, cudaStream_t);
-INST(float, 2)
-INST(float, 3)
-INST(double, 2)
-INST(double, 3)
+#define INST(T, OP)                                                                                          \
+  template cudaError_t launch_compact<T, OP>(const T*, int64_t, int64_t, const typename OP::Params&, T*, int64_t, \
+                                             int64_t*, int64_t, uint8_t*, int64_t*, void*, cudaStream_t);
+typedef BoxOp<float, 2> BoxF2;
+typedef BoxOp<float, 3> BoxF3;
+typedef BoxOp<double, 2> BoxD2;
+typedef BoxOp<double, 3> BoxD3;
+typedef HomogOp<float, false> HomF;
+typedef HomogOp<float, true> HomFN;
+typedef HomogOp<double, false> HomD;
+typedef HomogOp<double, true> HomDN;
+INST(float, BoxF2)
+INST(float, BoxF3)
+INST(double, BoxD2)
+INST(double, BoxD3)
+INST(float, HomF)
+INST(float, HomFN)
+INST(double, HomD)
+INST(double, HomDN)
 #undef INST
 
 }  // namespace clipseg

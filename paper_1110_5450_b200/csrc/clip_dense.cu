@@ -10,37 +10,38 @@
 
 namespace clipseg {
 
-template <typename T, int D>
-__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 3 : 2) clip_dense_kernel(const T* in, int64_t ld_in, int64_t n, Window<T, D> w,
-                                                         T* out, int64_t ld_out, uint8_t* flags) {
-  constexpr int V = Vec16<T>::N;
+template <typename T, class Op>
+__global__ void __launch_bounds__(256, (sizeof(T) == 4 && Op::IN != 8) ? 3 : 2)
+    clip_dense_kernel(const T* in, int64_t ld_in, int64_t n, typename Op::Params w, T* out, int64_t ld_out,
+                      uint8_t* flags) {
+  constexpr int V = Vec16<T>::N, IN = Op::IN, OUT = Op::OUT;
   const int64_t ngroups = (n + V - 1) / V;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  T nxt[2 * D][V];
+  T nxt[IN][V];
   if (g < ngroups) {
 #pragma unroll
-    for (int c = 0; c < 2 * D; ++c) load_vec<T>(in + c * ld_in + g * V, nxt[c]);
+    for (int c = 0; c < IN; ++c) load_vec<T>(in + c * ld_in + g * V, nxt[c]);
   }
   for (; g < ngroups; g += stride) {
     const int64_t i = g * V;
-    T plane[2 * D][V];
+    T plane[IN][V];
 #pragma unroll
-    for (int c = 0; c < 2 * D; ++c)
+    for (int c = 0; c < IN; ++c)
 #pragma unroll
       for (int v = 0; v < V; ++v) plane[c][v] = nxt[c][v];
     if (g + stride < ngroups) {  // next group's loads in flight while this one is clipped
 #pragma unroll
-      for (int c = 0; c < 2 * D; ++c) load_vec<T>(in + c * ld_in + (g + stride) * V, nxt[c]);
+      for (int c = 0; c < IN; ++c) load_vec<T>(in + c * ld_in + (g + stride) * V, nxt[c]);
     }
-    T res[2 * D][V];
-    const unsigned bits = clip_group<T, D, V, true>(plane, w, res);
+    T res[OUT][V];
+    const unsigned bits = Op::template group<V, true>(plane, w, res);
     uint32_t vis = 0;  // one flag byte per segment
 #pragma unroll
     for (int v = 0; v < V; ++v) vis |= ((bits >> v) & 1u) << (8 * v);
     if (i + V <= n) {
 #pragma unroll
-      for (int c = 0; c < 2 * D; ++c) store_vec<T>(out + c * ld_out + i, res[c]);
+      for (int c = 0; c < OUT; ++c) store_vec<T>(out + c * ld_out + i, res[c]);
       if (flags) {
         if (V == 4) *reinterpret_cast<uint32_t*>(flags + i) = vis;
         else *reinterpret_cast<uint16_t*>(flags + i) = (uint16_t)vis;
@@ -49,7 +50,7 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 3 : 2) clip_dense_kernel
       for (int v = 0; v < V; ++v) {
         if (i + v < n) {
 #pragma unroll
-          for (int c = 0; c < 2 * D; ++c) out[c * ld_out + i + v] = res[c][v];
+          for (int c = 0; c < OUT; ++c) out[c * ld_out + i + v] = res[c][v];
           if (flags) flags[i + v] = (uint8_t)((vis >> (8 * v)) & 1u);
         }
       }
@@ -57,30 +58,42 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 3 : 2) clip_dense_kernel
   }
 }
 
-template <typename T, int D>
-cudaError_t launch_dense(const T* in, int64_t ld_in, int64_t n, const Window<T, D>& w, T* out, int64_t ld_out,
-                         uint8_t* flags, cudaStream_t s) {
+template <typename T, class Op>
+cudaError_t launch_dense(const T* in, int64_t ld_in, int64_t n, const typename Op::Params& w, T* out,
+                         int64_t ld_out, uint8_t* flags, cudaStream_t s) {
   constexpr int V = Vec16<T>::N, NT = 256;
   static int blocks_per_sm = 0;  // cached device attribute
   if (!blocks_per_sm) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, clip_dense_kernel<T, D>, NT, 0);
+    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, clip_dense_kernel<T, Op>, NT, 0);
     if (e != cudaSuccess || blocks_per_sm < 1) blocks_per_sm = 1;
   }
   const int64_t ngroups = (n + V - 1) / V;
   const int64_t want = (ngroups + NT - 1) / NT;
   const int64_t cap = (int64_t)device_sm_count() * blocks_per_sm;
   const int grid = (int)(want < cap ? want : cap);
-  clip_dense_kernel<T, D><<<grid, NT, 0, s>>>(in, ld_in, n, w, out, ld_out, flags);
+  clip_dense_kernel<T, Op><<<grid, NT, 0, s>>>(in, ld_in, n, w, out, ld_out, flags);
   return cudaGetLastError();
 }
 
-template cudaError_t launch_dense<float, 2>(const float*, int64_t, int64_t, const Window<float, 2>&, float*,
-                                            int64_t, uint8_t*, cudaStream_t);
-template cudaError_t launch_dense<float, 3>(const float*, int64_t, int64_t, const Window<float, 3>&, float*,
-                                            int64_t, uint8_t*, cudaStream_t);
-template cudaError_t launch_dense<double, 2>(const double*, int64_t, int64_t, const Window<double, 2>&, double*,
-                                             int64_t, uint8_t*, cudaStream_t);
-template cudaError_t launch_dense<double, 3>(const double*, int64_t, int64_t, const Window<double, 3>&, double*,
-                                             int64_t, uint8_t*, cudaStream_t);
+#define INST(T, OP)                                                                                         \
+  template cudaError_t launch_dense<T, OP>(const T*, int64_t, int64_t, const typename OP::Params&, T*, int64_t, \
+                                           uint8_t*, cudaStream_t);
+typedef BoxOp<float, 2> BoxF2;
+typedef BoxOp<float, 3> BoxF3;
+typedef BoxOp<double, 2> BoxD2;
+typedef BoxOp<double, 3> BoxD3;
+typedef HomogOp<float, false> HomF;
+typedef HomogOp<float, true> HomFN;
+typedef HomogOp<double, false> HomD;
+typedef HomogOp<double, true> HomDN;
+INST(float, BoxF2)
+INST(float, BoxF3)
+INST(double, BoxD2)
+INST(double, BoxD3)
+INST(float, HomF)
+INST(float, HomFN)
+INST(double, HomD)
+INST(double, HomDN)
+#undef INST
 
 }  // namespace clipseg

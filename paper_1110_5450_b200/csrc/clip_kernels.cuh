@@ -8,6 +8,29 @@
 
 namespace clipseg {
 
+// A clip operation as the kernels see it: IN input planes, OUT output planes per segment,
+// the per-call parameters, and the group clip of V segments (returns the visible bits;
+// NAN_FILL writes R8's qNaN into invisible rows).
+template <typename T, int D> struct BoxOp {  // axis-aligned closed box, D = 2, 3 (rules R1..R10)
+  static constexpr int IN = 2 * D, OUT = 2 * D;
+  typedef Window<T, D> Params;
+  template <int V, bool NAN_FILL>
+  static __device__ __forceinline__ unsigned group(const T (&pl)[IN][V], const Params& w, T (&res)[OUT][V]) {
+    return clip_group<T, D, V, NAN_FILL>(pl, w, res);
+  }
+};
+struct NoParams {
+  int unused;
+};
+template <typename T, bool NDC> struct HomogOp {  // NEXT-1: homogeneous clip space (rules H1..H10)
+  static constexpr int IN = 8, OUT = NDC ? 6 : 8;
+  typedef NoParams Params;
+  template <int V, bool NAN_FILL>
+  static __device__ __forceinline__ unsigned group(const T (&pl)[IN][V], const Params&, T (&res)[OUT][V]) {
+    return homog_group<T, V, NAN_FILL, NDC>(pl, res);
+  }
+};
+
 // Workspace of the compacting kernel: a 128-byte header (tile-claim counter) followed by
 // one 64-bit look-back status word per tile.
 constexpr int kCompactThreads = 256;
@@ -33,33 +56,35 @@ template <typename T> __host__ __device__ constexpr int compact_items() { return
 #endif
 // fp32 2D (the bench workload): one block per SM, 16 compute warps, 4096-segment tiles,
 // 3 staged (~203 KB); fp32 3D: 16 warps, 2048-segment tiles; fp64: 8 compute warps and
-// 1024-segment tiles, so the wider rows keep enough registers.
-template <typename T, int D> __host__ __device__ constexpr bool compact_headline() {
-  return sizeof(T) == 4 && D == 2;
+// 1024-segment tiles, so the wider rows keep enough registers; homogeneous (8 input
+// planes): fp32 8 warps x 2048-segment tiles, fp64 4 warps x 1024.
+template <typename T, class Op> __host__ __device__ constexpr bool compact_headline() {
+  return sizeof(T) == 4 && Op::IN == 4;
 }
-template <typename T, int D> __host__ __device__ constexpr int compact_warps() {
-  return compact_headline<T, D>() ? CLIPSEG_COMPUTE_WARPS : (sizeof(T) == 4 ? 16 : 8);
+template <typename T, class Op> __host__ __device__ constexpr int compact_warps() {
+  return compact_headline<T, Op>() ? CLIPSEG_COMPUTE_WARPS
+                                   : (Op::IN == 8 ? (sizeof(T) == 4 ? 8 : 4) : (sizeof(T) == 4 ? 16 : 8));
 }
-template <typename T, int D> __host__ __device__ constexpr int compact_subtiles() {
-  return compact_headline<T, D>() ? CLIPSEG_NSUB_F32_2D : (sizeof(T) == 4 ? 16 : 8);
+template <typename T, class Op> __host__ __device__ constexpr int compact_subtiles() {
+  return compact_headline<T, Op>() ? CLIPSEG_NSUB_F32_2D : (sizeof(T) == 4 ? 16 : 8);
 }
-template <typename T, int D> __host__ __device__ constexpr int compact_buffers() {
-  return compact_headline<T, D>() ? CLIPSEG_NBUF_F32_2D : ((sizeof(T) == 8 && D == 3) ? 2 : 3);
+template <typename T, class Op> __host__ __device__ constexpr int compact_buffers() {
+  return compact_headline<T, Op>() ? CLIPSEG_NBUF_F32_2D : ((sizeof(T) == 8 && Op::IN == 6) ? 2 : 3);
 }
-template <typename T, int D> __host__ __device__ constexpr int compact_min_blocks() {
-  return compact_headline<T, D>() ? CLIPSEG_MINB_F32_2D : 1;
+template <typename T, class Op> __host__ __device__ constexpr int compact_min_blocks() {
+  return compact_headline<T, Op>() ? CLIPSEG_MINB_F32_2D : 1;
 }
 // Smallest block tile over all (T, D): the workspace is sized with it.
 constexpr int64_t kMinCompactTile = 8 * 128;
 
-template <typename T, int D>
-cudaError_t launch_dense(const T* in, int64_t ld_in, int64_t n, const Window<T, D>& w, T* out, int64_t ld_out,
-                         uint8_t* flags, cudaStream_t s);
+template <typename T, class Op>
+cudaError_t launch_dense(const T* in, int64_t ld_in, int64_t n, const typename Op::Params& w, T* out,
+                         int64_t ld_out, uint8_t* flags, cudaStream_t s);
 
-template <typename T, int D>
-cudaError_t launch_compact(const T* in, int64_t ld_in, int64_t n, const Window<T, D>& w, T* out, int64_t ld_out,
-                           int64_t* out_index, int64_t index_base, uint8_t* flags, int64_t* d_count, void* ws,
-                           cudaStream_t s);
+template <typename T, class Op>
+cudaError_t launch_compact(const T* in, int64_t ld_in, int64_t n, const typename Op::Params& w, T* out,
+                           int64_t ld_out, int64_t* out_index, int64_t index_base, uint8_t* flags, int64_t* d_count,
+                           void* ws, cudaStream_t s);
 
 cudaError_t launch_shard_offsets(const int64_t* d_counts, int P, int rank, int64_t* d_offset, int64_t* d_total,
                                  cudaStream_t s);

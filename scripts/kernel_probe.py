@@ -20,7 +20,8 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--dim", type=int, default=2)
     ap.add_argument("--dtype", choices=["f32", "f64"], default="f32")
-    ap.add_argument("--family", choices=["uniform", "mix10", "mix33", "mix90", "adv"], default="uniform")
+    ap.add_argument("--family", choices=["uniform", "mix10", "mix33", "mix90", "adv", "homog"], default="uniform")
+    ap.add_argument("--ndc", type=int, default=0, help="homog family: perspective-divided output")
     ap.add_argument("--flags", type=int, default=1)
     ap.add_argument("--index", type=int, default=0)
     a = ap.parse_args()
@@ -31,14 +32,17 @@ def main():
 
     dt = torch.float32 if a.dtype == "f32" else torch.float64
     esz = 4 if a.dtype == "f32" else 8
-    fam = {"uniform": synth.UNIFORM, "adv": synth.ADVERSARIAL}.get(a.family, synth.MIX)
+    fam = {"uniform": synth.UNIFORM, "adv": synth.ADVERSARIAL, "homog": synth.HOMOG}.get(a.family, synth.MIX)
+    homog = fam == synth.HOMOG
     mix = {"mix10": (0.10, 0.80), "mix33": (1 / 3, 1 / 3), "mix90": (0.90, 0.05)}.get(a.family, (0, 0))
     pin, pc = synth.mix_thresholds(*mix)
-    n, D = a.n, a.dim
+    n, D = a.n, (4 if homog else a.dim)
     planes = clipseg.empty_planes(n, D, dt)
     synth.fill_device(planes, fam, D, synth.seed_for(5), n, p_in=pin, p_cross=pc)
     lo, hi = [0.0] * D, [1.0] * D
     res = {"n": n, "dim": D, "dtype": a.dtype, "family": a.family}
+    IN = 2 * D
+    OUT = (6 if a.ndc else 8) if homog else 2 * D
     s = torch.cuda.current_stream()
 
     def timeit(fn):
@@ -56,17 +60,25 @@ def main():
         return statistics.median(ts), min(ts)
 
     if a.kernel in ("dense", "both"):
-        out = torch.empty_like(planes)
+        out = torch.empty((OUT, planes.shape[1]), dtype=dt, device="cuda")
         flags = torch.empty(n, dtype=torch.uint8, device="cuda") if a.flags else None
-        med, best = timeit(lambda: clipseg.clip(planes, n, lo, hi, out=out, flags=flags, want_flags=bool(a.flags)))
-        b = n * (2 * (2 * D * esz) + (1 if a.flags else 0))
+        if homog:
+            med, best = timeit(lambda: clipseg.clip_homog(planes, n, ndc=bool(a.ndc), out=out, flags=flags,
+                                                          want_flags=bool(a.flags)))
+        else:
+            med, best = timeit(lambda: clipseg.clip(planes, n, lo, hi, out=out, flags=flags, want_flags=bool(a.flags)))
+        b = n * ((IN + OUT) * esz + (1 if a.flags else 0))
         res["dense"] = {"ms": med, "best_ms": best, "GBps": b / med / 1e6, "seg_per_s": n / med * 1e3}
         del out
     if a.kernel in ("compact", "both"):
-        bufs = clipseg.CompactBuffers(n, D, dt, with_index=bool(a.index), with_flags=bool(a.flags))
-        med, best = timeit(lambda: clipseg.clip_compact(planes, n, lo, hi, bufs=bufs))
+        if homog:
+            bufs = clipseg.HomogBuffers(n, dt, bool(a.ndc), with_index=bool(a.index), with_flags=bool(a.flags))
+            med, best = timeit(lambda: clipseg.clip_homog_compact(planes, n, ndc=bool(a.ndc), bufs=bufs))
+        else:
+            bufs = clipseg.CompactBuffers(n, D, dt, with_index=bool(a.index), with_flags=bool(a.flags))
+            med, best = timeit(lambda: clipseg.clip_compact(planes, n, lo, hi, bufs=bufs))
         cnt = int(bufs.count.item())
-        b = n * (2 * D * esz + (1 if a.flags else 0)) + cnt * (2 * D * esz + (8 if a.index else 0))
+        b = n * (IN * esz + (1 if a.flags else 0)) + cnt * (OUT * esz + (8 if a.index else 0))
         res["compact"] = {"ms": med, "best_ms": best, "GBps": b / med / 1e6, "seg_per_s": n / med * 1e3,
                           "visible": cnt / n}
     print(json.dumps(res))

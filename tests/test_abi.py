@@ -97,6 +97,31 @@ def test_compact_validation(cs):
     assert call(args(inp=FAKE + 8)) == cs.CLIP_EALIGN
 
 
+def test_homog_validation(cs):
+    big = 1 << 30
+    f = cs.clip_homog_segments_f32
+    assert f(FAKE, 32, -1, 0, FAKE, 32, None, None) == cs.CLIP_EINVAL
+    assert f(FAKE, 32, 10, 2, FAKE, 32, None, None) == cs.CLIP_EINVAL            # ndc must be 0 / 1
+    assert f(FAKE, 32, 0, 1, FAKE, 32, None, None) == cs.CLIP_OK                 # n == 0: no launch
+    assert f(FAKE, 8, 10, 0, FAKE, 32, None, None) == cs.CLIP_EINVAL             # ld < n
+    assert f(FAKE + 4, 32, 10, 0, FAKE, 32, None, None) == cs.CLIP_EALIGN
+    assert f(FAKE, 32, 10, 0, FAKE, 32, FAKE + 2, None) == cs.CLIP_EALIGN
+    assert cs.clip_homog_segments_f64(FAKE, 33, 10, 0, FAKE, 32, None, None) == cs.CLIP_EALIGN
+    g = cs.clip_homog_segments_compact_f32
+    ok = dict(inp=FAKE, ldi=1024, n=1000, ndc=0, out=FAKE + big, ldo=1024, idx=None, base=0, fl=None,
+              cnt=FAKE + 2 * big, ws=FAKE + 3 * big, wsb=1 << 20)
+
+    def call(**k):
+        a = dict(ok, **k)
+        return g(a["inp"], a["ldi"], a["n"], a["ndc"], a["out"], a["ldo"], a["idx"], a["base"], a["fl"], a["cnt"],
+                 a["ws"], a["wsb"], None)
+    assert call(cnt=None) == cs.CLIP_EINVAL
+    assert call(ndc=-1) == cs.CLIP_EINVAL
+    assert call(wsb=64) == cs.CLIP_ENOSPACE
+    assert call(ws=FAKE + 3 * big + 8) == cs.CLIP_EALIGN
+    assert call(out=FAKE + 7 * 1024 * 4) == cs.CLIP_EINVAL                     # overlaps in's last plane
+
+
 def test_shard_offsets_validation(cs):
     assert cs.clip_shard_offsets(FAKE, 0, 0, FAKE, FAKE, None) == cs.CLIP_EINVAL
     assert cs.clip_shard_offsets(FAKE, 2, 2, FAKE, FAKE, None) == cs.CLIP_EINVAL
