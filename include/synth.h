@@ -13,7 +13,8 @@
  * family: 0 uniform grid in [-1,2)^dim, 1 inside/crossing/outside mix with
  * probabilities p_in/2^32 and p_cross/2^32 (the rest outside), 2 adversarial,
  * 3 homogeneous clip-space segments (dim must be 4: planes x0,y0,z0,w0,x1,y1,z1,w1;
- * tag = mode 0 perspective, 1 affine w = 1, 2 behind the eye, 3 on planes, 4 degenerate).
+ * tag = mode 0 perspective, 1 affine w = 1, 2 behind the eye, 3 on planes, 4 degenerate;
+ * p_in != 0 sets the perspective share to p_in/2^32, the other modes share the rest).
  * Returns SYNTH_OK (0) or a negative status; device variants launch
  * asynchronously on `stream` (a cudaStream_t, NULL = legacy default stream).
  */

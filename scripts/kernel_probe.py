@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--dtype", choices=["f32", "f64"], default="f32")
     ap.add_argument("--family", choices=["uniform", "mix10", "mix33", "mix90", "adv", "homog"], default="uniform")
     ap.add_argument("--ndc", type=int, default=0, help="homog family: perspective-divided output")
+    ap.add_argument("--persp", type=float, default=0.0, help="homog family: perspective share (0: recipe default)")
     ap.add_argument("--flags", type=int, default=1)
     ap.add_argument("--index", type=int, default=0)
     a = ap.parse_args()
@@ -36,11 +37,13 @@ def main():
     homog = fam == synth.HOMOG
     mix = {"mix10": (0.10, 0.80), "mix33": (1 / 3, 1 / 3), "mix90": (0.90, 0.05)}.get(a.family, (0, 0))
     pin, pc = synth.mix_thresholds(*mix)
+    if a.family == "homog" and a.persp > 0:
+        pin = synth.mix_thresholds(a.persp, 0)[0]
     n, D = a.n, (4 if homog else a.dim)
     planes = clipseg.empty_planes(n, D, dt)
     synth.fill_device(planes, fam, D, synth.seed_for(5), n, p_in=pin, p_cross=pc)
     lo, hi = [0.0] * D, [1.0] * D
-    res = {"n": n, "dim": D, "dtype": a.dtype, "family": a.family}
+    res = {"n": n, "dim": D, "dtype": a.dtype, "family": a.family, "persp": a.persp, "ndc": a.ndc}
     IN = 2 * D
     OUT = (6 if a.ndc else 8) if homog else 2 * D
     s = torch.cuda.current_stream()

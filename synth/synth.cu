@@ -12,7 +12,7 @@ namespace {
 // D == 4 is the homogeneous family (syn_homog); D = 2, 3 the cuboid families.
 template <typename T, int D>
 SYN_HD uint8_t gen_one(int family, uint64_t seed, int64_t i, uint32_t p_in, uint32_t p_cross, T (&p)[2 * D]) {
-  if constexpr (D == 4) return syn_homog<T>(seed, i, p);
+  if constexpr (D == 4) return syn_homog<T>(seed, i, p, p_in);
   else return syn_segment<T, D>(family, seed, i, p_in, p_cross, p);
 }
 

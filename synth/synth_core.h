@@ -258,12 +258,15 @@ SYN_HD uint8_t syn_segment(int family, uint64_t seed, int64_t i, uint32_t p_in, 
  *   10 % behind: one endpoint with w in (-2, -0.5];
  *   10 % on planes: one endpoint exactly on a plane (x = +-w) or an edge/corner of the volume;
  *   10 % degenerate: an endpoint with w = 0 (the 4D origin, or a random direction), or a
- *        zero-length segment. */
+ *        zero-length segment.
+ * A nonzero p_persp sets the perspective share to p_persp / 2^32 instead (bench workloads). */
 template <typename T>
-SYN_HD uint8_t syn_homog(uint64_t seed, int64_t i, T p[8]) {
+SYN_HD uint8_t syn_homog(uint64_t seed, int64_t i, T p[8], uint32_t p_persp) {
   typedef SynT<T> S;
   const uint64_t h0 = syn_h(seed, i, 15);
-  const int m = (int)((h0 >> 32) % 10u);
+  /* p_persp != 0 overrides the perspective share (p_persp / 2^32; the rest 6..9 equally) */
+  const int m = p_persp == 0u ? (int)((h0 >> 32) % 10u)
+                              : ((h0 >> 32) < (uint64_t)p_persp ? 0 : 6 + (int)((h0 >> 1) % 4u));
   for (int e = 0; e < 2; ++e) {
     for (int k = 0; k < 3; ++k) p[4 * e + k] = (T)2 * S::grid(syn_h(seed, i, 4 * e + k)) - (T)1;
     p[4 * e + 3] = (m == 6) ? (T)1 : S::wpos(syn_h(seed, i, 4 * e + 3));
