@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=40_000_000)
+    ap.add_argument("--no-next1", action="store_true", help="skip the secondary NEXT-1 (homogeneous) measurement")
     return ap.parse_args()
 
 
@@ -275,6 +276,11 @@ def main():
     # sampled parity of this run's output against the oracle (outside the timed region)
     parity = sampled_parity(torch, bufs, n, start, rank)
 
+    # secondary: the NEXT-1 row (homogeneous clip space), rank 0 at N = 1 only
+    next1 = None
+    if rank == 0 and world == 1 and not args.no_next1:
+        next1 = run_next1(torch, clipseg, synth, dev, stream)
+
     # end to end through the public host-buffer API (pinned host memory, H2D + D2H timed)
     e2e = None
     if not args.no_e2e:
@@ -311,6 +317,7 @@ def main():
         "e2e": e2e,
         "cpu_baseline": cpu,
         "parity": parity,
+        "next1": next1,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -338,6 +345,55 @@ def sampled_parity(torch, bufs, n, start, rank, m=2000):
     ok = ok and np.array_equal(got.view(np.uint32), want[:, vis].view(np.uint32))
     del pos
     return f"{'ok' if ok else 'MISMATCH'}: {len(idx)} sampled segments bit-exact vs oracle"
+
+
+def run_next1(torch, clipseg, synth, dev, stream, n=10**8, steps=20):
+    """NEXT-1: the compacting clip in homogeneous clip space, 1e8 fp32
+    segments of the HOMOG recipe, homogeneous output + flags; CUDA events on the launching
+    stream; roofline against the same measured HBM peak; sampled parity vs the oracle."""
+    import numpy as np  # noqa: PLC0415
+    import oracle  # noqa: PLC0415
+    seed = synth.seed_for(6)
+    planes = torch.empty((8, clipseg.clip_plane_stride(n)), dtype=torch.float32, device=dev)
+    synth.fill_device(planes, synth.HOMOG, 4, seed, n)
+    bufs = clipseg.HomogBuffers(n, torch.float32, False, dev, with_flags=True)
+    for _ in range(3):
+        clipseg.clip_homog_compact(planes, n, bufs=bufs, stream=stream)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in ev:
+        a.record(stream)
+        clipseg.clip_homog_compact(planes, n, bufs=bufs, stream=stream)
+        b.record(stream)
+    torch.cuda.synchronize()
+    ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+    cnt = int(bufs.count.item())
+    alg = n * (8 * 4 + 1) + cnt * 8 * 4
+    peak, _ = measured_peak()
+    # sampled parity: flags and compacted rows of 2000 segments vs the oracle
+    rng = np.random.default_rng(7)
+    idx = np.unique(np.concatenate([rng.integers(0, n, 2000), [0, n - 1]]))
+    P = np.zeros((8, synth.plane_stride(len(idx))), np.float32)
+    for j, i in enumerate(idx):
+        p, _ = synth.fill_host(synth.HOMOG, 4, seed, 1, i0=int(i), nthreads=1, with_tag=False)
+        P[:, j] = p[:, 0]
+    want, wfl = oracle.homog_clip(P, len(idx))
+    fl = bufs.flags[:n]
+    ti = torch.from_numpy(idx).to(dev)
+    ok = np.array_equal(fl[ti].cpu().numpy(), wfl)
+    pos = torch.cumsum(fl, 0, dtype=torch.int32) - 1
+    vis = np.nonzero(wfl)[0]
+    got = bufs.out[:, pos[ti[torch.from_numpy(vis).to(dev)]].long()].cpu().numpy()
+    ok = ok and np.array_equal(got.view(np.uint32), want[:, vis].view(np.uint32))
+    del planes, bufs, pos
+    return {"workload": "NEXT-1: homogeneous clip space (-w <= x,y,z <= w), compacting clip, 1e8 fp32 segments "
+                        "(HOMOG recipe: 60% perspective, 10% each affine / behind / on-plane / degenerate), "
+                        "homogeneous output + flags",
+            "value": n / (ms / 1e3), "unit": "segments/s", "ms": ms, "visible_fraction": cnt / n,
+            "roofline": {"bound": "hbm", "achieved": alg / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": alg / (ms / 1e3) / 1e9 / peak, "kernel": "clip_compact_kernel<float,HomogOp>",
+                         "alg_bytes_per_launch": alg},
+            "parity": f"{'ok' if ok else 'MISMATCH'}: {len(idx)} sampled segments bit-exact vs oracle"}
 
 
 def run_e2e(torch, dist, clipseg, synth, args, world, rank, dev):
