@@ -170,34 +170,44 @@ __device__ __noinline__ void global_scanner(unsigned long long* status, int64_t 
 
 }  // namespace
 
-template <typename T, class Op> struct CompactShape {
+#ifndef CLIPSEG_PITCH_PAD
+#define CLIPSEG_PITCH_PAD 0  // extra staged rows per plane beyond SUB + 1 (0: the scratch row only)
+#endif
+constexpr size_t kMaxSmemPerBlock = 227 * 1024 - 2048;  // dynamic smem budget (static smem aside)
+
+template <typename T, class Op, bool INDEX> struct CompactShape {
   static constexpr int V = Vec16<T>::N;                 // segments per 128-bit vector
   static constexpr int IT = compact_items<T>();          // vectors per lane per sub-tile
   static constexpr int SUB = 32 * V * IT;                // 128 segments per sub-tile
   static constexpr int NSUB = compact_subtiles<T, Op>();  // sub-tiles per block tile
   static constexpr int BT = NSUB * SUB;
-  static constexpr int NBUF = compact_buffers<T, Op>();   // staged tiles in flight per block
-  static constexpr int PITCH = SUB + V;                  // staged plane pitch: rows + scratch row
+  static constexpr int PITCH = SUB + 1 + CLIPSEG_PITCH_PAD;  // staged plane pitch: rows + scratch row
   static constexpr int SLOT = Op::OUT * PITCH;           // staged elements per sub-tile
+  // per staged tile: the rows, plus the local indices when out_index is requested
+  static constexpr size_t kBufBytes = (size_t)NSUB * SLOT * sizeof(T) + (INDEX ? (size_t)NSUB * (SUB + 1) : 0);
+  static constexpr int NBUF = (size_t)compact_buffers<T, Op>() * kBufBytes <= kMaxSmemPerBlock
+                                  ? compact_buffers<T, Op>()
+                                  : (int)(kMaxSmemPerBlock / kBufBytes);  // staged tiles in flight
   static constexpr size_t kStageBytes = (size_t)NBUF * NSUB * SLOT * sizeof(T);
-  static constexpr size_t kSmemBytes = kStageBytes + (size_t)NBUF * NSUB * (SUB + 1);  // + local indices
+  static constexpr size_t kSmemBytes = (size_t)NBUF * kBufBytes;
   static constexpr int kMinBlocks = compact_min_blocks<T, Op>();
   static constexpr int kComputeWarps = compact_warps<T, Op>();
   static constexpr int kThreads = (kComputeWarps + 1) * 32;  // + the scan warp
 };
 
 template <typename T, class Op, bool FLAGS, bool INDEX>
-__global__ void __launch_bounds__(CompactShape<T, Op>::kThreads, CompactShape<T, Op>::kMinBlocks) clip_compact_kernel(
+__global__ void __launch_bounds__(CompactShape<T, Op, INDEX>::kThreads, CompactShape<T, Op, INDEX>::kMinBlocks)
+    clip_compact_kernel(
     const T* __restrict__ in, int64_t ld_in, int64_t n, typename Op::Params w, T* __restrict__ out, int64_t ld_out,
     int64_t* __restrict__ out_index, int64_t index_base, uint8_t* __restrict__ flags, int64_t* __restrict__ d_count,
     unsigned long long* __restrict__ ws, int64_t ntiles) {
-  typedef CompactShape<T, Op> S;
+  typedef CompactShape<T, Op, INDEX> S;
   constexpr int IN = Op::IN, OUT = Op::OUT;
   constexpr int V = S::V, IT = S::IT, SUB = S::SUB, NSUB = S::NSUB, BT = S::BT, SLOT = S::SLOT, NBUF = S::NBUF;
   constexpr int PITCH = S::PITCH;
   constexpr int kComputeWarps = S::kComputeWarps;
   constexpr int PER_WARP = NSUB / kComputeWarps;
-  static_assert(NSUB % kComputeWarps == 0 && NSUB <= 32 && NBUF >= 2 && NBUF <= kTileRing - 2, "tile layout");
+  static_assert(NSUB % kComputeWarps == 0 && NSUB <= 64 && NBUF >= 2 && NBUF <= kTileRing - 2, "tile layout");
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* stage = reinterpret_cast<T*>(smem_raw);            // [NBUF][NSUB][2D][SUB]
@@ -245,15 +255,21 @@ __global__ void __launch_bounds__(CompactShape<T, Op>::kThreads, CompactShape<T,
       const int64_t tile = s_tile[k & kRingMask];
       if (tile >= ntiles) break;
       mbar_wait_sleepy(&mb_cnt[b], (par >> b) & 1u, 256);  // the compute warps' counts of tile k
-      const int c = (lane < NSUB) ? s_cnt[b][lane] : 0;
+      // lane holds sub-tiles lane and lane + 32, packed in the low / high 16 bits (a tile
+      // count is at most 32 x 128 < 2^16)
+      const int c0 = (lane < NSUB) ? s_cnt[b][lane] : 0;
+      const int c1 = (NSUB > 32 && lane + 32 < NSUB) ? s_cnt[b][lane + 32] : 0;
+      const int c = c0 | (c1 << 16);
       int incl = c;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const int y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
         if (lane >= d) incl += y;
       }
-      if (lane < NSUB) s_pre[b][lane] = incl - c;
-      const int64_t total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      const int tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      if (lane < NSUB) s_pre[b][lane] = (incl & 0xFFFF) - c0;
+      if (NSUB > 32 && lane + 32 < NSUB) s_pre[b][lane + 32] = (tot & 0xFFFF) + (incl >> 16) - c1;
+      const int64_t total = (tot & 0xFFFF) + (tot >> 16);
       if (lane == 0) {
         CLIP_TRACE(tile, 3, trace_now());
         unsigned long long st;
@@ -427,6 +443,7 @@ __global__ void __launch_bounds__(CompactShape<T, Op>::kThreads, CompactShape<T,
       if (last) {
         __threadfence_block();
         int c = (lane < NSUB) ? ((volatile int*)s_cnt[b])[lane] : 0;
+        if (NSUB > 32 && lane + 32 < NSUB) c += ((volatile int*)s_cnt[b])[lane + 32];
 #pragma unroll
         for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, d);
         if (lane == 0) {
@@ -495,7 +512,7 @@ template <typename T, class Op, bool FLAGS, bool INDEX>
 static cudaError_t launch_compact_variant(const T* in, int64_t ld_in, int64_t n, const typename Op::Params& w, T* out,
                                          int64_t ld_out, int64_t* out_index, int64_t index_base, uint8_t* flags,
                                          int64_t* d_count, unsigned long long* ws, int64_t ntiles, cudaStream_t s) {
-  typedef CompactShape<T, Op> S;
+  typedef CompactShape<T, Op, INDEX> S;
   const size_t smem = S::kSmemBytes;
   auto kern = clip_compact_kernel<T, Op, FLAGS, INDEX>;
   static int blocks_per_sm = 0;  // cached device attribute
@@ -518,7 +535,7 @@ template <typename T, class Op>
 cudaError_t launch_compact(const T* in, int64_t ld_in, int64_t n, const typename Op::Params& w, T* out,
                            int64_t ld_out, int64_t* out_index, int64_t index_base, uint8_t* flags, int64_t* d_count,
                            void* ws, cudaStream_t s) {
-  typedef CompactShape<T, Op> S;
+  typedef CompactShape<T, Op, false> S;  // the tile size does not depend on out_index
   const int64_t ntiles = (n + S::BT - 1) / S::BT;
   cudaError_t e = cudaMemsetAsync(ws, 0, kWsHeaderBytes + (size_t)ntiles * 8, s);
   if (e != cudaSuccess) return e;
