@@ -16,7 +16,8 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libclip_oracle.so")
+# CLIP_ORACLE_LIB: a mutated build of the same oracle (scripts/mutate_oracle.py only)
+_SO = os.environ.get("CLIP_ORACLE_LIB") or os.path.join(_HERE, "libclip_oracle.so")
 _lib = None
 _lock = threading.Lock()
 
