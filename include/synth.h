@@ -38,6 +38,14 @@ int synth_fill_device_f32(int family, int dim, uint64_t seed, int64_t i0, int64_
 int synth_fill_device_f64(int family, int dim, uint64_t seed, int64_t i0, int64_t n, double* planes, int64_t ld,
                           uint8_t* tag, uint32_t p_in, uint32_t p_cross, void* stream);
 
+/* NEXT-2 input: n pixels of batched ToF frames (ppf pixels per frame),
+ * global pixel index i0 + r -> d[r] (meters, 0 = invalid), I[r] (intensity, I = rho / d^2);
+ * synth_tof_ranges: the per-frame clip range r[2f] = r_min, r[2f+1] = r_max of frames
+ * f0 .. f0 + nframes - 1 (host). */
+int synth_tof_host(uint64_t seed, int64_t i0, int64_t n, int64_t ppf, float* d, float* I, int nthreads);
+int synth_tof_device(uint64_t seed, int64_t i0, int64_t n, int64_t ppf, float* d, float* I, void* stream);
+int synth_tof_ranges(uint64_t seed, int64_t f0, int64_t nframes, float* r);
+
 #ifdef __cplusplus
 }
 #endif

@@ -56,6 +56,12 @@ def lib():
                 f = getattr(L, "synth_fill_device_" + s)
                 f.argtypes = [ctypes.c_int, ctypes.c_int, U64, I64, I64, P, I64, P, U32, U32, P]
                 f.restype = ctypes.c_int
+            L.synth_tof_host.argtypes = [U64, I64, I64, I64, P, P, ctypes.c_int]
+            L.synth_tof_host.restype = ctypes.c_int
+            L.synth_tof_device.argtypes = [U64, I64, I64, I64, P, P, P]
+            L.synth_tof_device.restype = ctypes.c_int
+            L.synth_tof_ranges.argtypes = [U64, I64, I64, P]
+            L.synth_tof_ranges.restype = ctypes.c_int
             _lib = L
     return _lib
 
@@ -88,3 +94,35 @@ def fill_device(planes_t, family, dim, seed, n, i0=0, p_in=0, p_cross=0, tag_t=N
            p_in, p_cross, stream)
     if st != 0:
         raise RuntimeError(f"synth_fill_device: status {st}")
+
+
+# ---- NEXT-2: batched ToF frames -------------------------------------------
+TOF_W = TOF_H = 204            # 204^2 pixel frames
+TOF_PPF = TOF_W * TOF_H
+
+
+def tof_host(seed, nframes, ppf=TOF_PPF, f0=0, nthreads=None):
+    """Frames f0 .. f0+nframes-1 on the host: (d float32[n], I float32[n], ranges float32[nframes, 2])."""
+    n = nframes * ppf
+    d = np.empty(max(n, 1), np.float32)
+    I = np.empty(max(n, 1), np.float32)
+    r = np.empty((max(nframes, 1), 2), np.float32)
+    nthreads = nthreads or min(8, os.cpu_count() or 1)
+    assert lib().synth_tof_host(seed, f0 * ppf, n, ppf, d.ctypes.data, I.ctypes.data, nthreads) == 0
+    assert lib().synth_tof_ranges(seed, f0, nframes, r.ctypes.data) == 0
+    return d[:n], I[:n], r[:nframes]
+
+
+def tof_device(d_t, I_t, seed, nframes, ppf=TOF_PPF, f0=0, stream=None):
+    """Fill CUDA float32 tensors d_t, I_t (>= nframes*ppf elements) asynchronously; returns the
+    per-frame ranges as a host float32 array (nframes, 2)."""
+    import torch  # noqa: PLC0415
+    n = nframes * ppf
+    if stream is None:
+        stream = torch.cuda.current_stream().cuda_stream
+    st = lib().synth_tof_device(seed, f0 * ppf, n, ppf, d_t.data_ptr(), I_t.data_ptr(), stream)
+    if st != 0:
+        raise RuntimeError(f"synth_tof_device: status {st}")
+    r = np.empty((max(nframes, 1), 2), np.float32)
+    assert lib().synth_tof_ranges(seed, f0, nframes, r.ctypes.data) == 0
+    return r[:nframes]

@@ -77,9 +77,51 @@ int check(int family, int dim, int64_t i0, int64_t n, const void* planes, int64_
   return SYNTH_OK;
 }
 
+void tof_host_range(uint64_t seed, int64_t i0, int64_t a, int64_t b, int64_t ppf, float* d, float* I) {
+  for (int64_t r = a; r < b; ++r) syn_tof_pixel(seed, i0 + r, ppf, d + r, I + r);
+}
+
+__global__ void tof_kernel(uint64_t seed, int64_t i0, int64_t n, int64_t ppf, float* __restrict__ d,
+                           float* __restrict__ I) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n; r += stride)
+    syn_tof_pixel(seed, i0 + r, ppf, d + r, I + r);
+}
+
 }  // namespace
 
 extern "C" {
+
+int synth_tof_host(uint64_t seed, int64_t i0, int64_t n, int64_t ppf, float* d, float* I, int nthreads) {
+  if (n < 0 || i0 < 0 || ppf <= 0 || (n > 0 && (!d || !I))) return SYNTH_EINVAL;
+  if (nthreads <= 1 || n < (1 << 16)) {
+    tof_host_range(seed, i0, 0, n, ppf, d, I);
+    return SYNTH_OK;
+  }
+  std::vector<std::thread> th;
+  for (int t = 0; t < nthreads; ++t)
+    th.emplace_back(tof_host_range, seed, i0, n * t / nthreads, n * (t + 1) / nthreads, ppf, d, I);
+  for (auto& x : th) x.join();
+  return SYNTH_OK;
+}
+
+int synth_tof_device(uint64_t seed, int64_t i0, int64_t n, int64_t ppf, float* d, float* I, void* stream) {
+  if (n < 0 || i0 < 0 || ppf <= 0 || (n > 0 && (!d || !I))) return SYNTH_EINVAL;
+  if (n == 0) return SYNTH_OK;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t want = (n + 255) / 256;
+  const int grid = (int)(want < (int64_t)sms * 16 ? want : (int64_t)sms * 16);
+  tof_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(seed, i0, n, ppf, d, I);
+  return cudaGetLastError() == cudaSuccess ? SYNTH_OK : SYNTH_ECUDA;
+}
+
+int synth_tof_ranges(uint64_t seed, int64_t f0, int64_t nframes, float* r) {
+  if (nframes < 0 || f0 < 0 || (nframes > 0 && !r)) return SYNTH_EINVAL;
+  for (int64_t f = 0; f < nframes; ++f) syn_tof_range(seed, f0 + f, r + 2 * f);
+  return SYNTH_OK;
+}
 
 int synth_fill_host_f32(int family, int dim, uint64_t seed, int64_t i0, int64_t n, float* planes, int64_t ld,
                         uint8_t* tag, uint32_t p_in, uint32_t p_cross, int nthreads) {

@@ -293,3 +293,46 @@ SYN_HD uint8_t syn_homog(uint64_t seed, int64_t i, T p[8], uint32_t p_persp) {
   else { for (int k = 0; k < 4; ++k) p[4 * (1 - e) + k] = P[k]; }         /* zero length */
   return SYN_H_DEGENERATE;
 }
+
+/* ---- NEXT-2 input: batched ToF frames (distance d, intensity I per pixel) -------------
+ * PAPER.md §5.2 clips pixels to [r_min, r_max] per frame; Eq. (5) fuses
+ * them into phi = arctan(d sqrt(I)) under the inverse-square law I ~ 1/d^2.  Frames
+ * are 204 x 204 in the paper.  Per pixel (global index i, draws j = 0..3):
+ *   2 % dropouts (d = I = 0, the invalid sentinel); 40 % "hand" pixels within +-0.2 m of one
+ *   of the frame's two hand distances; 58 % background, d uniform in [0.3, 7.5) m; d is a
+ *   multiple of 2^-20 m; intensity I = rho / (d d), reflectivity rho in [0.2, 1) (the constant
+ *   c of SPEC.md:400 makes I(1 m, rho = 1) = 1).
+ * Per frame f: hand distances d1, d2 in [0.5, 1.5) and the clip range r_min = max(1e-3,
+ * min(d1, d2) - r_th), r_max = max(d1, d2) + r_th with r_th = 0.1 m (§5.2 formulas;
+ * r_th from Table 1 via SPEC.md:262). */
+SYN_HD float syn_tof_hand(uint64_t seed, int64_t f, int which) {
+  const uint64_t h = syn_h(seed ^ 0x70F0C11Bull, f, which);
+  return 0.5f + (float)(h & 0xFFFFFull) * 0x1p-20f;   /* [0.5, 1.5) on a 2^-20 grid */
+}
+
+SYN_HD void syn_tof_range(uint64_t seed, int64_t f, float r[2]) {
+  const float d1 = syn_tof_hand(seed, f, 0), d2 = syn_tof_hand(seed, f, 1);
+  const float lo = (d1 < d2 ? d1 : d2) - 0.1f, hi = (d1 < d2 ? d2 : d1) + 0.1f;
+  r[0] = lo > 1e-3f ? lo : 1e-3f;
+  r[1] = hi;
+}
+
+SYN_HD void syn_tof_pixel(uint64_t seed, int64_t i, int64_t ppf, float* d, float* I) {
+  const uint64_t h0 = syn_h(seed, i, 0), h1 = syn_h(seed, i, 1), h2 = syn_h(seed, i, 2);
+  const uint32_t u = (uint32_t)(h0 >> 32) % 100u;
+  if (u < 2u) { *d = 0.0f; *I = 0.0f; return; }
+  float dist;
+  if (u < 42u) {
+    const float dh = syn_tof_hand(seed, i / ppf, (int)(h0 & 1u));
+    /* hand pixel: dh + k 2^-20, |k 2^-20| < 0.2 (dh is on the 2^-20 grid: exact) */
+    const int32_t k = (int32_t)(h1 % 419430ull) - 209715;
+    dist = dh + (float)k * 0x1p-20f;
+  } else {
+    /* background: [0.3, 7.5) m on the 2^-20 grid */
+    const uint32_t k = 314573u + (uint32_t)(h1 % 7549747ull);
+    dist = (float)k * 0x1p-20f;
+  }
+  const float rho = 0.2f + (float)(h2 & 0xFFFFFull) * (0.8f * 0x1p-20f);
+  *d = dist;
+  *I = rho / (dist * dist);
+}
