@@ -139,6 +139,22 @@ int clip_homog_segments_compact_f64(const double* in, int64_t ld_in, int64_t n, 
                                     int64_t ld_out, int64_t* out_index, int64_t index_base, uint8_t* flags,
                                     int64_t* d_count, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ---- NEXT-2: the paper's per-pixel step — range clip + fused measure ---
+ * PAPER.md §5.2: "pixels outside the range [r_min, r_max] will be ignored for
+ * clustering", the range recomputed per frame; §4.2 Eq. (5): phi = arctan(d sqrt(I)).
+ * d, I:    n pixels (device, 16-byte aligned): radial distance (m; 0 = invalid / dropout) and
+ *          intensity, frames of pix_per_frame consecutive pixels (the last may be ragged).
+ * ranges:  device float[2 * F], F = ceil(n / pix_per_frame): r_min, r_max of each frame.
+ * phi:     n floats (16-byte aligned): arctan(d sqrt(I)) in binary32 for kept pixels, the
+ *          canonical qNaN otherwise.  phi must not overlap d or I.
+ * code:    (nullable, 4-byte aligned) n bytes: 4 invalid (d <= 0, non-finite d or I, I < 0),
+ *          else bit 0 = d < r_min, bit 1 = d > r_max; kept iff 0 (closed interval).
+ * kept:    (nullable, 4-byte aligned) int32[F]: kept pixels per frame (zeroed by the call).
+ * Status: CLIP_EINVAL (n < 0 or n >= 2^52, pix_per_frame < 1, null d/I/ranges/phi), CLIP_EALIGN,
+ * CLIP_ECUDA; n == 0 launches nothing. */
+int clip_tof_range_phi_f32(const float* d, const float* I, int64_t n, int64_t pix_per_frame, const float* ranges,
+                           float* phi, uint8_t* code, int32_t* kept, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

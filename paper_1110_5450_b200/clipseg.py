@@ -52,6 +52,8 @@ def _load():
         f = getattr(L, "clip_homog_segments_compact_" + s)
         f.argtypes = [P, I64, I64, ctypes.c_int, P, I64, P, I64, U8P, P, P, SZ, P]
         f.restype = ctypes.c_int
+    L.clip_tof_range_phi_f32.argtypes = [P, P, I64, I64, P, P, U8P, P, P]
+    L.clip_tof_range_phi_f32.restype = ctypes.c_int
     L.clip_compact_workspace_bytes.argtypes = [I64]
     L.clip_compact_workspace_bytes.restype = SZ
     L.clip_host_staging_bytes.argtypes = [ctypes.c_int, ctypes.c_int, I64]
@@ -75,6 +77,7 @@ clip_shard_offsets = _lib.clip_shard_offsets
 clip_host_staging_bytes = _lib.clip_host_staging_bytes
 clip_segments_compact_host_f32 = _lib.clip_segments_compact_host_f32
 clip_segments_compact_host_f64 = _lib.clip_segments_compact_host_f64
+clip_tof_range_phi_f32 = _lib.clip_tof_range_phi_f32
 clip_homog_segments_f32 = _lib.clip_homog_segments_f32
 clip_homog_segments_f64 = _lib.clip_homog_segments_f64
 clip_homog_segments_compact_f32 = _lib.clip_homog_segments_compact_f32
@@ -84,7 +87,7 @@ EXPORTED = ["clip_plane_stride", "clip_status_string", "clip_segments_f32", "cli
             "clip_compact_workspace_bytes", "clip_segments_compact_f32", "clip_segments_compact_f64",
             "clip_shard_offsets", "clip_host_staging_bytes", "clip_segments_compact_host_f32",
             "clip_segments_compact_host_f64", "clip_homog_segments_f32", "clip_homog_segments_f64",
-            "clip_homog_segments_compact_f32", "clip_homog_segments_compact_f64"]
+            "clip_homog_segments_compact_f32", "clip_homog_segments_compact_f64", "clip_tof_range_phi_f32"]
 
 
 class ClipError(RuntimeError):
@@ -249,6 +252,26 @@ def clip_homog_compact(planes, n, ndc=False, bufs: HomogBuffers | None = None, w
              bufs.flags.data_ptr() if bufs.flags is not None else None, bufs.count.data_ptr(),
              bufs.ws.data_ptr(), bufs.ws.numel(), _stream(stream)), "clip_homog_segments_compact_" + sfx)
     return bufs
+
+
+# ---- NEXT-2: range clip + phi over batched ToF frames ----------------------------------------
+def tof_range_phi(d, I, ppf, ranges, phi=None, code=None, kept=None, want_code=True, want_kept=True, stream=None):
+    """d, I: CUDA float32[n]; ranges: CUDA float32[F, 2] (r_min, r_max per frame).
+    Returns (phi float32[n], code uint8[n] or None, kept int32[F] or None)."""
+    torch = _torch()
+    n = d.numel()
+    nf = (n + ppf - 1) // ppf
+    if phi is None:
+        phi = torch.empty(max(n, 4), dtype=torch.float32, device=d.device)
+    if code is None and want_code:
+        code = torch.empty(max(n, 4), dtype=torch.uint8, device=d.device)
+    if kept is None and want_kept:
+        kept = torch.empty(max(nf, 1), dtype=torch.int32, device=d.device)
+    _check(clip_tof_range_phi_f32(d.data_ptr(), I.data_ptr(), n, ppf, ranges.data_ptr(), phi.data_ptr(),
+                                  code.data_ptr() if code is not None else None,
+                                  kept.data_ptr() if kept is not None else None, _stream(stream)),
+           "clip_tof_range_phi_f32")
+    return phi, code, kept
 
 
 def shard_offsets(counts_t, rank, stream=None):

@@ -329,6 +329,17 @@ int clip_segments_compact_host_f64(const double* h_in, int64_t ld_in, int64_t n,
   return compact_host<double>(h_in, ld_in, n, win, h_out, ld_out, h_flags, h_count, chunk, d_staging, staging_bytes);
 }
 
+int clip_tof_range_phi_f32(const float* d, const float* I, int64_t n, int64_t pix_per_frame, const float* ranges,
+                           float* phi, uint8_t* code, int32_t* kept, void* stream) {
+  if (n < 0 || n >= ((int64_t)1 << 52) || pix_per_frame < 1) return CLIP_EINVAL;
+  if (n == 0) return CLIP_OK;
+  if (!d || !I || !ranges || !phi) return CLIP_EINVAL;
+  if (!aligned(d, 16) || !aligned(I, 16) || !aligned(phi, 16) || !aligned(ranges, 4)) return CLIP_EALIGN;
+  if ((code && !aligned(code, 4)) || (kept && !aligned(kept, 4))) return CLIP_EALIGN;
+  return status_of(launch_tof_range_phi(d, I, n, pix_per_frame, ranges, phi, code, reinterpret_cast<int*>(kept),
+                                        reinterpret_cast<cudaStream_t>(stream)));
+}
+
 int clip_homog_segments_f32(const float* in, int64_t ld_in, int64_t n, int ndc, float* out, int64_t ld_out,
                             uint8_t* flags, void* stream) {
   return homog_dense<float>(in, ld_in, n, ndc, out, ld_out, flags, stream);

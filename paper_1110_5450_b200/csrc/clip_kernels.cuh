@@ -89,6 +89,10 @@ cudaError_t launch_compact(const T* in, int64_t ld_in, int64_t n, const typename
 cudaError_t launch_shard_offsets(const int64_t* d_counts, int P, int rank, int64_t* d_offset, int64_t* d_total,
                                  cudaStream_t s);
 
+// NEXT-2 (tof_range.cu): range clip + phi over batched frames of ppf pixels.
+cudaError_t launch_tof_range_phi(const float* d, const float* I, int64_t n, int64_t ppf, const float* ranges,
+                                 float* phi, uint8_t* code, int* kept, cudaStream_t s);
+
 // Number of SMs of the current device (cached per device).
 int device_sm_count();
 

@@ -122,6 +122,19 @@ def test_homog_validation(cs):
     assert call(out=FAKE + 7 * 1024 * 4) == cs.CLIP_EINVAL                     # overlaps in's last plane
 
 
+def test_tof_validation(cs):
+    f = cs.clip_tof_range_phi_f32
+    assert f(FAKE, FAKE, -1, 10, FAKE, FAKE, None, None, None) == cs.CLIP_EINVAL
+    assert f(FAKE, FAKE, 10, 0, FAKE, FAKE, None, None, None) == cs.CLIP_EINVAL      # ppf < 1
+    assert f(FAKE, FAKE, 0, 10, FAKE, FAKE, None, None, None) == cs.CLIP_OK          # n == 0: no launch
+    assert f(None, FAKE, 10, 10, FAKE, FAKE, None, None, None) == cs.CLIP_EINVAL
+    assert f(FAKE, FAKE, 10, 10, None, FAKE, None, None, None) == cs.CLIP_EINVAL
+    assert f(FAKE + 4, FAKE, 10, 10, FAKE, FAKE, None, None, None) == cs.CLIP_EALIGN
+    assert f(FAKE, FAKE, 10, 10, FAKE, FAKE + 8, None, None, None) == cs.CLIP_EALIGN
+    assert f(FAKE, FAKE, 10, 10, FAKE, FAKE, FAKE + 2, None, None) == cs.CLIP_EALIGN
+    assert f(FAKE, FAKE, 10, 10, FAKE, FAKE, None, FAKE + 2, None) == cs.CLIP_EALIGN
+
+
 def test_shard_offsets_validation(cs):
     assert cs.clip_shard_offsets(FAKE, 0, 0, FAKE, FAKE, None) == cs.CLIP_EINVAL
     assert cs.clip_shard_offsets(FAKE, 2, 2, FAKE, FAKE, None) == cs.CLIP_EINVAL
