@@ -155,6 +155,32 @@ int clip_homog_segments_compact_f64(const double* in, int64_t ld_in, int64_t n, 
 int clip_tof_range_phi_f32(const float* d, const float* I, int64_t n, int64_t pix_per_frame, const float* ranges,
                            float* phi, uint8_t* code, int32_t* kept, void* stream);
 
+/* ---- NEXT-3: the paper's GPU hot path — mutual-best region merging ------
+ * PAPER.md §4.1: every valid pixel starts as a region (id = row-major pixel
+ * index + 1 within its frame); each round every region picks the 4-adjacent region that
+ * passes Eq. (1) (|dz| <= t_z and |dphi| <= t_phi) with the smallest Eq. (2) difference
+ * alpha_z |dz| + alpha_phi |dphi|, ties to the larger id (rule 2); mutual choices merge
+ * (rule 3) into the larger id with pixel-count-weighted mean descriptors; all
+ * choices of a round use the state at its start; rounds repeat until one merges nothing.
+ * Table 1 parameters: t_z = 0.04 m, t_phi = 0.009 rad, alpha_z = 8/pi, alpha_phi = 4/3.
+ * z, phi:   nframes * height * width binary32 values per pixel (device, row-major frames);
+ * valid:    bytes, nonzero = the pixel is a region (0: invalid / clipped, label 0);
+ * labels:   int32 per pixel: the id of its final region (0 for invalid pixels);
+ * nregions: (nullable) int32[nframes] final region counts; d_rounds: (nullable) device int32:
+ *           rounds run including the final one without merges (max_rounds if not converged);
+ * workspace: clip_cluster_workspace_bytes(...) device bytes, 256-byte aligned.
+ * Limits: nframes * height * width < 2^30.  Status: CLIP_EINVAL (bad sizes, negative or
+ * non-finite params, max_rounds < 1, null pointers), CLIP_EALIGN, CLIP_ENOSPACE, CLIP_ECUDA.
+ * One cooperative launch (the rounds run on the device, no host round trips). */
+typedef struct {
+  double t_z, t_phi, alpha_z, alpha_phi;
+} clip_merge_params;
+size_t clip_cluster_workspace_bytes(int64_t nframes, int height, int width);
+int clip_cluster_frames(const float* z, const float* phi, const uint8_t* valid, int64_t nframes, int height,
+                        int width, const clip_merge_params* params, int max_rounds, int32_t* labels,
+                        int32_t* nregions, int32_t* d_rounds, void* workspace, size_t workspace_bytes,
+                        void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -26,6 +26,14 @@ class clip_window_f64(ctypes.Structure):  # noqa: N801
     _fields_ = [("lo", ctypes.c_double * 3), ("hi", ctypes.c_double * 3), ("dim", ctypes.c_int)]
 
 
+class clip_merge_params(ctypes.Structure):  # noqa: N801
+    _fields_ = [("t_z", ctypes.c_double), ("t_phi", ctypes.c_double), ("alpha_z", ctypes.c_double),
+                ("alpha_phi", ctypes.c_double)]
+
+
+TABLE1 = dict(t_z=0.04, t_phi=0.009, alpha_z=8 / 3.141592653589793, alpha_phi=4 / 3)  # PAPER Table 1
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"libclipseg.so not built at {LIB_PATH}: run `python build_all.py` "
@@ -54,6 +62,11 @@ def _load():
         f.restype = ctypes.c_int
     L.clip_tof_range_phi_f32.argtypes = [P, P, I64, I64, P, P, U8P, P, P]
     L.clip_tof_range_phi_f32.restype = ctypes.c_int
+    L.clip_cluster_workspace_bytes.argtypes = [I64, ctypes.c_int, ctypes.c_int]
+    L.clip_cluster_workspace_bytes.restype = SZ
+    L.clip_cluster_frames.argtypes = [P, P, P, I64, ctypes.c_int, ctypes.c_int, ctypes.POINTER(clip_merge_params),
+                                      ctypes.c_int, P, P, P, P, SZ, P]
+    L.clip_cluster_frames.restype = ctypes.c_int
     L.clip_compact_workspace_bytes.argtypes = [I64]
     L.clip_compact_workspace_bytes.restype = SZ
     L.clip_host_staging_bytes.argtypes = [ctypes.c_int, ctypes.c_int, I64]
@@ -78,6 +91,8 @@ clip_host_staging_bytes = _lib.clip_host_staging_bytes
 clip_segments_compact_host_f32 = _lib.clip_segments_compact_host_f32
 clip_segments_compact_host_f64 = _lib.clip_segments_compact_host_f64
 clip_tof_range_phi_f32 = _lib.clip_tof_range_phi_f32
+clip_cluster_workspace_bytes = _lib.clip_cluster_workspace_bytes
+clip_cluster_frames = _lib.clip_cluster_frames
 clip_homog_segments_f32 = _lib.clip_homog_segments_f32
 clip_homog_segments_f64 = _lib.clip_homog_segments_f64
 clip_homog_segments_compact_f32 = _lib.clip_homog_segments_compact_f32
@@ -87,7 +102,8 @@ EXPORTED = ["clip_plane_stride", "clip_status_string", "clip_segments_f32", "cli
             "clip_compact_workspace_bytes", "clip_segments_compact_f32", "clip_segments_compact_f64",
             "clip_shard_offsets", "clip_host_staging_bytes", "clip_segments_compact_host_f32",
             "clip_segments_compact_host_f64", "clip_homog_segments_f32", "clip_homog_segments_f64",
-            "clip_homog_segments_compact_f32", "clip_homog_segments_compact_f64", "clip_tof_range_phi_f32"]
+            "clip_homog_segments_compact_f32", "clip_homog_segments_compact_f64", "clip_tof_range_phi_f32",
+            "clip_cluster_workspace_bytes", "clip_cluster_frames"]
 
 
 class ClipError(RuntimeError):
@@ -272,6 +288,29 @@ def tof_range_phi(d, I, ppf, ranges, phi=None, code=None, kept=None, want_code=T
                                   kept.data_ptr() if kept is not None else None, _stream(stream)),
            "clip_tof_range_phi_f32")
     return phi, code, kept
+
+
+# ---- NEXT-3: mutual-best region merging of batched frames -----------------------------------
+def cluster_frames(z, phi, valid, params=None, max_rounds=1 << 30, labels=None, workspace=None, stream=None):
+    """z, phi: CUDA float32[F, H, W]; valid: CUDA uint8/bool[F, H, W].  Returns (labels int32[F, H, W],
+    nregions int32[F], rounds (device int32[1]), workspace)."""
+    torch = _torch()
+    F, H, W = z.shape
+    p = dict(TABLE1, **(params or {}))
+    prm = clip_merge_params(p["t_z"], p["t_phi"], p["alpha_z"], p["alpha_phi"])
+    if valid.dtype == torch.bool:
+        valid = valid.to(torch.uint8)
+    if labels is None:
+        labels = torch.empty((F, H, W), dtype=torch.int32, device=z.device)
+    nregions = torch.empty(max(F, 1), dtype=torch.int32, device=z.device)
+    rounds = torch.zeros(1, dtype=torch.int32, device=z.device)
+    need = int(clip_cluster_workspace_bytes(F, H, W))
+    if workspace is None or workspace.numel() < need:
+        workspace = torch.empty(max(need, 256), dtype=torch.uint8, device=z.device)
+    _check(clip_cluster_frames(z.data_ptr(), phi.data_ptr(), valid.data_ptr(), F, H, W, ctypes.byref(prm),
+                               min(max_rounds, 2**31 - 1), labels.data_ptr(), nregions.data_ptr(), rounds.data_ptr(),
+                               workspace.data_ptr(), workspace.numel(), _stream(stream)), "clip_cluster_frames")
+    return labels, nregions[:F], rounds, workspace
 
 
 def shard_offsets(counts_t, rank, stream=None):

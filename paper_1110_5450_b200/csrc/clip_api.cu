@@ -340,6 +340,32 @@ int clip_tof_range_phi_f32(const float* d, const float* I, int64_t n, int64_t pi
                                         reinterpret_cast<cudaStream_t>(stream)));
 }
 
+size_t clip_cluster_workspace_bytes(int64_t nframes, int height, int width) {
+  if (nframes < 0 || height < 1 || width < 1) return 0;
+  return cluster_workspace_bytes(nframes * (int64_t)height * width) + 4096;
+}
+
+int clip_cluster_frames(const float* z, const float* phi, const uint8_t* valid, int64_t nframes, int height,
+                        int width, const clip_merge_params* params, int max_rounds, int32_t* labels,
+                        int32_t* nregions, int32_t* d_rounds, void* workspace, size_t workspace_bytes,
+                        void* stream) {
+  if (nframes < 0 || height < 1 || width < 1 || !params || max_rounds < 1) return CLIP_EINVAL;
+  const int64_t n = nframes * (int64_t)height * width;
+  if (n >= ((int64_t)1 << 31) / 2) return CLIP_EINVAL;  // int region and edge indices
+  if (!(params->t_z >= 0) || !(params->t_phi >= 0) || !(params->alpha_z >= 0) || !(params->alpha_phi >= 0) ||
+      !std::isfinite(params->t_z + params->t_phi + params->alpha_z + params->alpha_phi))
+    return CLIP_EINVAL;
+  if (n == 0) return CLIP_OK;
+  if (!z || !phi || !valid || !labels || !workspace) return CLIP_EINVAL;
+  if (!aligned(z, 4) || !aligned(phi, 4) || !aligned(labels, 4) || !aligned(workspace, 256) ||
+      (nregions && !aligned(nregions, 4)) || (d_rounds && !aligned(d_rounds, 4)))
+    return CLIP_EALIGN;
+  if (workspace_bytes < clip_cluster_workspace_bytes(nframes, height, width)) return CLIP_ENOSPACE;
+  return status_of(launch_cluster(z, phi, valid, nframes, height, width, params->t_z, params->t_phi,
+                                  params->alpha_z, params->alpha_phi, max_rounds, labels, nregions, d_rounds,
+                                  workspace, reinterpret_cast<cudaStream_t>(stream)));
+}
+
 int clip_homog_segments_f32(const float* in, int64_t ld_in, int64_t n, int ndc, float* out, int64_t ld_out,
                             uint8_t* flags, void* stream) {
   return homog_dense<float>(in, ld_in, n, ndc, out, ld_out, flags, stream);
