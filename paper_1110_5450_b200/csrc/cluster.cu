@@ -4,15 +4,19 @@
 //
 // One persistent cooperative kernel runs every round; grid-wide barriers separate the
 // phases of a round (the paper's Find Mergepartner / Merge Regions / Update Values, Table 2):
-//   A  edges:   Eq. (1) test and Eq. (2) distance on the frozen means; per endpoint the
-//               minimum distance (64-bit atomicMin on the non-negative double's bits);
-//   B  edges:   among the allowed neighbours at that minimum, the largest id (rule 2);
-//   C  regions: mutual pairs (rule 3): the smaller id is absorbed (parent = partner), the
-//               larger id adds the partner's count and fp64 sums and refreshes its means;
-//   D  regions / edges: reset the choices; edges of absorbed regions move to the survivor,
-//               edges that became self-loops die.
-// A round that merges nothing ends the loop.  Finally pointer jumping resolves every
-// pixel's surviving region id.  Region g of the batch is pixel g (frame g / P, id g % P + 1).
+//   A  live edges: move the endpoints absorbed last round to their survivors (one hop), drop
+//      self-loops, append the edge to the next live list; Eq. (1) test and Eq. (2)
+//      distance on the frozen means; per endpoint the minimum distance (64-bit atomicMin on
+//      the non-negative double's bits);
+//   B  live edges: among the allowed neighbours at that minimum, the largest id (rule 2);
+//   C  live regions: mutual pairs (rule 3): the smaller id is absorbed (parent = partner), the
+//      larger adds the partner's count and fp64 sums and refreshes its means; the survivors
+//      and the unmatched form the next live list.
+// The live lists shrink with the graph (append order is irrelevant: every decision is an
+// order-free min / max / pair test), the per-round choice arrays are double-buffered so the
+// next round's are reset while this round's are read, and a round that merges nothing ends
+// the loop.  Finally pointer jumping resolves every pixel's surviving region id.  Region g of
+// the batch is pixel g (frame g / P, id g % P + 1).
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -27,18 +31,18 @@ namespace clipseg {
 namespace {
 
 struct ClusterWs {  // views into the caller's workspace, n = nframes * P regions
-  int* cnt;                  // pixels of region g (0: not a region / absorbed)
-  int* parent;               // g, or the region that absorbed g
-  int* bestid;               // rule 2 choice (partner id), 0 = none
-  int* ea;                   // edge endpoints (2 slots per pixel: right, down), -1 = dead
-  int* eb;
-  int* merges;               // [2] merged pairs of the current / next round
-  int* changed;              // pointer-jumping flag
-  double* sz;                // fp64 sums of the pixels' binary32 z and phi (DESIGN M-b)
+  int* cnt;                     // pixels of region g
+  int* parent;                  // g, or the region that absorbed g
+  int* bestid[2];               // rule 2 choice (partner id, 0 = none), per round parity
+  unsigned long long* bestd[2]; // minimum Eq. (2) distance (bits of a non-negative double)
+  int* ea[2];                   // live edge lists (endpoints), per round parity
+  int* eb[2];
+  int* rl[2];                   // live region lists, per round parity
+  int* counts;                  // [0..1] live edges, [2..3] live regions, [4..5] merges, [6] flag
+  double* sz;                   // fp64 sums of the pixels' binary32 z and phi (DESIGN M-b)
   double* sp;
-  double* mz;                // means sz / cnt, sp / cnt
+  double* mz;                   // means sz / cnt, sp / cnt
   double* mp;
-  unsigned long long* bestd; // minimum Eq. (2) distance (bits of a non-negative double)
 };
 
 struct MergeParams {
@@ -51,22 +55,38 @@ __device__ __forceinline__ bool eq1(const ClusterWs& w, int a, int b, const Merg
   return dz <= p.t_z && dp <= p.t_phi;                                         // Eq. (1)
 }
 
+// Warp-aggregated append: one atomic per warp; returns this lane's slot (if pred).
+__device__ __forceinline__ int append_slot(int* counter, bool pred) {
+  const unsigned act = __activemask();
+  const unsigned m = __ballot_sync(act, pred);
+  if (m == 0) return -1;
+  const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(counter, __popc(m));
+  base = __shfl_sync(act, base, leader);
+  return base + __popc(m & ((1u << lane) - 1u));
+}
+
 __global__ void __launch_bounds__(256) cluster_kernel(const float* __restrict__ z, const float* __restrict__ phi,
                                                        const uint8_t* __restrict__ valid, int64_t nframes, int H,
                                                        int W, MergeParams prm, ClusterWs w, int max_rounds,
                                                        int* __restrict__ labels, int* __restrict__ nregions,
                                                        int* __restrict__ rounds_out) {
   cg::grid_group grid = cg::this_grid();
-  const int64_t P = (int64_t)H * W, n = nframes * P, ne = 2 * n;
+  const int64_t P = (int64_t)H * W, n = nframes * P;
   const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  int* const ecount = w.counts;
+  int* const rcount = w.counts + 2;
+  int* const merges = w.counts + 4;
+  int* const changed = w.counts + 6;
 
-  // init: one region per valid pixel; edges to the right and lower valid neighbours
+  // init: one region per valid pixel, the live lists of round 0
   for (int64_t g = t0; g < n; g += stride) {
     const bool v = valid[g] != 0;
     w.cnt[g] = v;
     w.parent[g] = (int)g;
-    w.bestid[g] = 0;
-    w.bestd[g] = ~0ull;
+    w.bestid[0][g] = 0;
+    w.bestd[0][g] = ~0ull;
     const double zz = v ? (double)z[g] : 0.0, pp = v ? (double)phi[g] : 0.0;
     w.sz[g] = zz;
     w.sp[g] = pp;
@@ -75,54 +95,69 @@ __global__ void __launch_bounds__(256) cluster_kernel(const float* __restrict__ 
     const int64_t q = g % P;
     const int x = (int)(q % W), y = (int)(q / W);
     const bool r = v && x + 1 < W && valid[g + 1] != 0, d = v && y + 1 < H && valid[g + W] != 0;
-    w.ea[2 * g] = r ? (int)g : -1;
-    w.eb[2 * g] = (int)(g + 1);
-    w.ea[2 * g + 1] = d ? (int)g : -1;
-    w.eb[2 * g + 1] = (int)(g + W);
-  }
-  if (t0 == 0) {
-    w.merges[0] = 0;
-    w.merges[1] = 0;
+    int slot = append_slot(ecount + 0, r);
+    if (r) {
+      w.ea[0][slot] = (int)g;
+      w.eb[0][slot] = (int)(g + 1);
+    }
+    slot = append_slot(ecount + 0, d);
+    if (d) {
+      w.ea[0][slot] = (int)g;
+      w.eb[0][slot] = (int)(g + W);
+    }
+    slot = append_slot(rcount + 0, v);
+    if (v) w.rl[0][slot] = (int)g;
   }
   grid.sync();
 
   int round = 0;
   for (; round < max_rounds; ++round) {
-    // A: minimum Eq. (2) distance over the allowed neighbours
+    const int cur = round & 1, nxt = cur ^ 1;
+    // A: remap + compact the live edges; minimum Eq. (2) distance over allowed neighbours
+    const int ne = ecount[cur];
+    if (t0 == 0) rcount[nxt] = 0;  // last read by the previous round's phase C loop bound
     for (int64_t e = t0; e < ne; e += stride) {
-      const int a = w.ea[e];
-      if (a < 0) continue;
-      const int b = w.eb[e];
+      const int a = w.parent[w.ea[cur][e]], b = w.parent[w.eb[cur][e]];
+      const bool live = a != b;
+      const int slot = append_slot(ecount + nxt, live);
+      if (!live) continue;
+      w.ea[nxt][slot] = a;
+      w.eb[nxt][slot] = b;
       double dist;
       if (eq1(w, a, b, prm, &dist)) {
         const unsigned long long bits = (unsigned long long)__double_as_longlong(dist);
-        atomicMin(w.bestd + a, bits);
-        atomicMin(w.bestd + b, bits);
+        atomicMin(w.bestd[cur] + a, bits);
+        atomicMin(w.bestd[cur] + b, bits);
       }
     }
     grid.sync();
     // B: the largest id among the neighbours at that distance (rule 2)
-    for (int64_t e = t0; e < ne; e += stride) {
-      const int a = w.ea[e];
-      if (a < 0) continue;
-      const int b = w.eb[e];
+    const int ne2 = ecount[nxt];
+    if (t0 == 0) ecount[cur] = 0;  // the list just read becomes the next round's output
+    for (int64_t e = t0; e < ne2; e += stride) {
+      const int a = w.ea[nxt][e], b = w.eb[nxt][e];
       double dist;
       if (eq1(w, a, b, prm, &dist)) {
         const unsigned long long bits = (unsigned long long)__double_as_longlong(dist);
-        if (bits == w.bestd[a]) atomicMax(w.bestid + a, (int)(b % P) + 1);
-        if (bits == w.bestd[b]) atomicMax(w.bestid + b, (int)(a % P) + 1);
+        if (bits == w.bestd[cur][a]) atomicMax(w.bestid[cur] + a, (int)(b % P) + 1);
+        if (bits == w.bestd[cur][b]) atomicMax(w.bestid[cur] + b, (int)(a % P) + 1);
       }
     }
     grid.sync();
-    // C: mutual pairs merge into the larger id (rules 3)
-    for (int64_t g = t0; g < n; g += stride) {
-      const int bi = w.bestid[g];
-      if (bi == 0 || w.cnt[g] == 0) continue;
-      const int64_t base = g - g % P, me = (int)(g % P) + 1, pg = base + bi - 1;
-      if (w.bestid[pg] != me) continue;  // not mutual: wait
-      if (me < bi) {
-        w.parent[g] = (int)pg;  // absorbed; its count and sums stay readable for the survivor
-      } else {
+    // C: mutual pairs merge into the larger id (rule 3); the next live region list
+    const int nr = rcount[cur];
+    if (t0 == 0) merges[nxt] = 0;
+    for (int64_t i = t0; i < nr; i += stride) {
+      const int g = w.rl[cur][i];
+      const int bi = w.bestid[cur][g];
+      const int64_t base = g - g % P;
+      const int me = (int)(g % P) + 1;
+      const int pg = (int)(base + bi - 1);
+      const bool mutual = bi != 0 && w.bestid[cur][pg] == me;
+      const bool absorbed = mutual && me < bi;
+      if (absorbed) {
+        w.parent[g] = pg;  // its count and sums stay readable for the survivor
+      } else if (mutual) {
         const int c = w.cnt[g] + w.cnt[pg];
         const double s1 = __dadd_rn(w.sz[g], w.sz[pg]), s2 = __dadd_rn(w.sp[g], w.sp[pg]);
         w.cnt[g] = c;
@@ -130,37 +165,23 @@ __global__ void __launch_bounds__(256) cluster_kernel(const float* __restrict__ 
         w.sp[g] = s2;
         w.mz[g] = __ddiv_rn(s1, (double)c);
         w.mp[g] = __ddiv_rn(s2, (double)c);
-        atomicAdd(w.merges + (round & 1), 1);
+        atomicAdd(merges + cur, 1);
+      }
+      const int slot = append_slot(rcount + nxt, !absorbed);
+      if (!absorbed) {
+        w.rl[nxt][slot] = g;
+        w.bestid[nxt][g] = 0;  // the next round's choices (last used two rounds ago)
+        w.bestd[nxt][g] = ~0ull;
       }
     }
     grid.sync();
-    // D: reset choices, retire absorbed regions, move their edges to the survivors
-    for (int64_t g = t0; g < n; g += stride) {
-      w.bestid[g] = 0;
-      w.bestd[g] = ~0ull;
-      if (w.parent[g] != (int)g && w.cnt[g] != 0) w.cnt[g] = 0;  // absorbed this round
-    }
-    for (int64_t e = t0; e < ne; e += stride) {
-      const int a = w.ea[e];
-      if (a < 0) continue;
-      const int b = w.eb[e];
-      const int a2 = w.parent[a], b2 = w.parent[b];  // one hop: a survivor's parent is itself
-      if (a2 == b2) {
-        w.ea[e] = -1;
-      } else if (a2 != a || b2 != b) {
-        w.ea[e] = a2;
-        w.eb[e] = b2;
-      }
-    }
-    if (t0 == 0) w.merges[(round + 1) & 1] = 0;
-    grid.sync();
-    if (w.merges[round & 1] == 0) break;  // the same value for every thread: uniform exit
+    if (merges[cur] == 0) break;  // the same value for every thread: uniform exit
   }
   if (t0 == 0 && rounds_out) *rounds_out = round < max_rounds ? round + 1 : max_rounds;
 
   // labels: pointer jumping to the surviving region, then its id (0 for invalid pixels)
   for (;;) {
-    if (t0 == 0) *w.changed = 0;
+    if (t0 == 0) *changed = 0;
     grid.sync();
     int ch = 0;
     for (int64_t g = t0; g < n; g += stride) {
@@ -170,9 +191,9 @@ __global__ void __launch_bounds__(256) cluster_kernel(const float* __restrict__ 
         ch = 1;
       }
     }
-    if (ch) atomicOr(w.changed, 1);
+    if (ch) atomicOr(changed, 1);
     grid.sync();
-    if (*w.changed == 0) break;
+    if (*changed == 0) break;
     grid.sync();  // everyone has read the flag before it is reset
   }
   for (int64_t g = t0; g < n; g += stride) {
@@ -186,7 +207,8 @@ __global__ void __launch_bounds__(256) cluster_kernel(const float* __restrict__ 
 }  // namespace
 
 size_t cluster_workspace_bytes(int64_t n) {
-  return (size_t)n * (4 * 3 + 4 * 4 + 8 * 5) + 64;  // cnt/parent/bestid, ea/eb, sums/means/bestd
+  // sums/means 4 x 8, choices 2 x (8 + 4), cnt/parent 2 x 4, edges 2 x 2 x 2 x 4, regions 2 x 4
+  return (size_t)n * (32 + 24 + 8 + 32 + 8) + 16 * 256;
 }
 
 cudaError_t launch_cluster(const float* z, const float* phi, const uint8_t* valid, int64_t nframes, int H, int W,
@@ -204,14 +226,20 @@ cudaError_t launch_cluster(const float* z, const float* phi, const uint8_t* vali
   w.sp = reinterpret_cast<double*>(take(8 * n));
   w.mz = reinterpret_cast<double*>(take(8 * n));
   w.mp = reinterpret_cast<double*>(take(8 * n));
-  w.bestd = reinterpret_cast<unsigned long long*>(take(8 * n));
+  for (int q = 0; q < 2; ++q) {
+    w.bestd[q] = reinterpret_cast<unsigned long long*>(take(8 * n));
+    w.bestid[q] = reinterpret_cast<int*>(take(4 * n));
+    w.ea[q] = reinterpret_cast<int*>(take(8 * n));
+    w.eb[q] = reinterpret_cast<int*>(take(8 * n));
+    w.rl[q] = reinterpret_cast<int*>(take(4 * n));
+  }
   w.cnt = reinterpret_cast<int*>(take(4 * n));
   w.parent = reinterpret_cast<int*>(take(4 * n));
-  w.bestid = reinterpret_cast<int*>(take(4 * n));
-  w.ea = reinterpret_cast<int*>(take(8 * n));
-  w.eb = reinterpret_cast<int*>(take(8 * n));
-  w.merges = reinterpret_cast<int*>(take(16));
-  w.changed = w.merges + 2;
+  w.counts = reinterpret_cast<int*>(take(64));
+  {
+    const cudaError_t e = cudaMemsetAsync(w.counts, 0, 64, s);
+    if (e != cudaSuccess) return e;
+  }
   MergeParams prm{t_z, t_phi, alpha_z, alpha_phi};
   if (nregions) {
     const cudaError_t e = cudaMemsetAsync(nregions, 0, (size_t)nframes * sizeof(int), s);

@@ -80,3 +80,10 @@ def test_all_invalid_and_tiny(torch, cs):
     v[1, 1, 1] = True
     lab, nreg, rounds = run(torch, cs, z, z, v)
     assert lab[0].sum() == 0 and nreg.tolist() == [0, 1] and lab[1, 1, 1] == 5 and rounds == 1
+
+
+def test_full_size_frames(torch, cs):
+    """Two 204 x 204 frames (the paper's sensor): ~1000 rounds each, labels identical."""
+    z, ph, v, gt = scenes.batch(2, 204, 204, seed=11)
+    lab = check(torch, cs, z, ph, v)
+    assert 2 <= len(np.unique(lab[0])) <= 50
