@@ -483,7 +483,7 @@ def run_next3(torch, clipseg, dev, stream, nframes=64, steps=3):
             "value": nframes / (ms / 1e3), "unit": "frames/s", "ms_per_batch": ms, "ms_per_frame": ms / nframes,
             "rounds": nr, "us_per_round": ms * 1e3 / max(nr, 1),
             "mean_regions_per_frame": float(nreg.float().mean().item()),
-            "roofline": {"bound": "latency (grid barriers: 4 per round, ~1000 rounds)",
+            "roofline": {"bound": "latency (3 grid barriers per round, ~1800 rounds)",
                          "achieved": io_bytes / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": io_bytes / (ms / 1e3) / 1e9 / peak, "kernel": "cluster_kernel",
                          "alg_bytes_per_launch": io_bytes},
