@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--no-next1", action="store_true", help="skip the secondary NEXT-1 (homogeneous) measurement")
     ap.add_argument("--no-next2", action="store_true", help="skip the secondary NEXT-2 (range clip + phi) measurement")
     ap.add_argument("--no-next3", action="store_true", help="skip the secondary NEXT-3 (region merging) measurement")
+    ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE.json configs[0..3] sweep")
     return ap.parse_args()
 
 
@@ -285,6 +286,9 @@ def main():
     next2 = None
     if rank == 0 and world == 1 and not args.no_next2:
         next2 = run_next2(torch, clipseg, synth, dev, stream)
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        configs = run_config_sweep(torch, clipseg, synth, dev, stream)
     next3 = None
     if rank == 0 and world == 1 and not args.no_next3:
         next3 = run_next3(torch, clipseg, dev, stream)
@@ -325,6 +329,7 @@ def main():
         "e2e": e2e,
         "cpu_baseline": cpu,
         "parity": parity,
+        "configs": configs,
         "next1": next1,
         "next2": next2,
         "next3": next3,
@@ -355,6 +360,58 @@ def sampled_parity(torch, bufs, n, start, rank, m=2000):
     ok = ok and np.array_equal(got.view(np.uint32), want[:, vis].view(np.uint32))
     del pos
     return f"{'ok' if ok else 'MISMATCH'}: {len(idx)} sampled segments bit-exact vs oracle"
+
+
+def run_config_sweep(torch, clipseg, synth, dev, stream, steps=10):
+    """BASELINE.json configs[0..3] at one GPU, beside the C5 headline:
+    the compacting (flags on) and dense kernels, CUDA events, algorithmic bytes / HBM peak."""
+    peak, _ = measured_peak()
+    rows = []
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(steps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    cases = [("C1 2D fp32 1e4 uniform", synth.UNIFORM, 2, torch.float32, 10**4, (0, 0)),
+             ("C2 2D fp32 1e8 mix 10/80/10", synth.MIX, 2, torch.float32, 10**8, (0.10, 0.80)),
+             ("C2 2D fp32 1e8 mix 33/33/33", synth.MIX, 2, torch.float32, 10**8, (1 / 3, 1 / 3)),
+             ("C2 2D fp32 1e8 mix 90/5/5", synth.MIX, 2, torch.float32, 10**8, (0.90, 0.05)),
+             ("C2 2D fp32 1e8 uniform", synth.UNIFORM, 2, torch.float32, 10**8, (0, 0)),
+             ("C3 2D fp32 1e7 adversarial", synth.ADVERSARIAL, 2, torch.float32, 10**7, (0, 0)),
+             ("C3 2D fp64 1e7 adversarial", synth.ADVERSARIAL, 2, torch.float64, 10**7, (0, 0)),
+             ("C4 3D fp32 1e8 uniform", synth.UNIFORM, 3, torch.float32, 10**8, (0, 0))]
+    for name, fam, D, dt, n, mix in cases:
+        esz = 4 if dt == torch.float32 else 8
+        pin, pc = synth.mix_thresholds(*mix)
+        planes = clipseg.empty_planes(n, D, dt, dev)
+        synth.fill_device(planes, fam, D, synth.seed_for(2), n, p_in=pin, p_cross=pc)
+        lo, hi = [0.0] * D, [1.0] * D
+        bufs = clipseg.CompactBuffers(n, D, dt, dev, with_flags=True)
+        ms_c = timed(lambda: clipseg.clip_compact(planes, n, lo, hi, bufs=bufs, stream=stream))
+        cnt = int(bufs.count.item())
+        del bufs
+        out = torch.empty_like(planes)
+        flags = torch.empty(n, dtype=torch.uint8, device=dev)
+        ms_d = timed(lambda: clipseg.clip(planes, n, lo, hi, out=out, flags=flags, stream=stream))
+        del out, flags, planes
+        bc = n * (2 * D * esz + 1) + cnt * 2 * D * esz
+        bd = n * (4 * D * esz + 1)
+        rows.append({"config": name, "visible_fraction": cnt / n,
+                     "compact": {"ms": ms_c, "segments_per_s": n / ms_c * 1e3, "GBps": bc / ms_c / 1e6,
+                                 "frac": bc / ms_c / 1e6 / peak},
+                     "dense": {"ms": ms_d, "segments_per_s": n / ms_d * 1e3, "GBps": bd / ms_d / 1e6,
+                               "frac": bd / ms_d / 1e6 / peak}})
+    return rows
 
 
 def run_next1(torch, clipseg, synth, dev, stream, n=10**8, steps=20):
