@@ -62,6 +62,15 @@ constexpr unsigned long long kFlagA = 1ull << 62;
 constexpr unsigned long long kFlagP = 2ull << 62;
 constexpr unsigned long long kValueMask = (1ull << 62) - 1;
 constexpr int kScanPerLane = 16;                     // scanner: 512 tiles per probe
+#ifndef CLIPSEG_POLL_NS
+#define CLIPSEG_POLL_NS 500        // scan warp: sleep between polls of its tile's prefix
+#endif
+#ifndef CLIPSEG_SCAN_SLEEP_NS
+#define CLIPSEG_SCAN_SLEEP_NS 256  // scan warp: sleep between tests of its mbarriers
+#endif
+#ifndef CLIPSEG_STORE_HINT
+#define CLIPSEG_STORE_HINT 0       // copy-out stores: 0 evict-first (st.cs), 1 plain
+#endif
 // Claimed-tile ring: a slot is rewritten kTileRing iterations after its first use; it must
 // exceed the copy lag (NBUF - 1) by enough that no warp still reads the old id.
 constexpr int kTileRing = 8, kRingMask = kTileRing - 1;
@@ -251,10 +260,10 @@ __global__ void __launch_bounds__(CompactShape<T, Op, INDEX>::kThreads, CompactS
     int b = 0;
     unsigned par = 0;  // bit q: parity of the next phase of mb_cnt[q] / mb_pre[q]
     for (int64_t k = 0;; ++k) {
-      mbar_wait_sleepy(&mb_tile[k & kRingMask], (uint32_t)((k / kTileRing) & 1), 256);
+      mbar_wait_sleepy(&mb_tile[k & kRingMask], (uint32_t)((k / kTileRing) & 1), CLIPSEG_SCAN_SLEEP_NS);
       const int64_t tile = s_tile[k & kRingMask];
       if (tile >= ntiles) break;
-      mbar_wait_sleepy(&mb_cnt[b], (par >> b) & 1u, 256);  // the compute warps' counts of tile k
+      mbar_wait_sleepy(&mb_cnt[b], (par >> b) & 1u, CLIPSEG_SCAN_SLEEP_NS);  // the compute warps' counts of tile k
       // lane holds sub-tiles lane and lane + 32, packed in the low / high 16 bits (a tile
       // count is at most 32 x 128 < 2^16)
       const int c0 = (lane < NSUB) ? s_cnt[b][lane] : 0;
@@ -274,7 +283,7 @@ __global__ void __launch_bounds__(CompactShape<T, Op, INDEX>::kThreads, CompactS
         CLIP_TRACE(tile, 3, trace_now());
         unsigned long long st;
         while (((st = ld_relaxed(status + tile)) >> 62) != 2u)  // the scanner's inclusive prefix
-          __nanosleep(500);  // it typically lands several microseconds after the aggregate
+          __nanosleep(CLIPSEG_POLL_NS);  // it typically lands several microseconds after the aggregate
         CLIP_TRACE(tile, 4, trace_now());
         CLIP_TRACE(tile, 7, blockIdx.x);
         s_prefix[b] = (int64_t)(st & kValueMask) - total;
@@ -475,7 +484,13 @@ __global__ void __launch_bounds__(CompactShape<T, Op, INDEX>::kThreads, CompactS
           const T* src = st + c * PITCH + lane;
 #pragma unroll
           for (int q = 0; q < SUB / 32; ++q)
-            if (q * 32 + lane < cnt) __stcs(dst + q * 32, src[q * 32]);
+            if (q * 32 + lane < cnt) {
+#if CLIPSEG_STORE_HINT == 1
+              dst[q * 32] = src[q * 32];
+#else
+              __stcs(dst + q * 32, src[q * 32]);
+#endif
+            }
         }
         if (INDEX) {
           const int64_t ib = index_base + pend[Q] * BT + (int64_t)sub * SUB;

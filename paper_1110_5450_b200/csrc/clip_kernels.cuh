@@ -61,15 +61,74 @@ template <typename T> __host__ __device__ constexpr int compact_items() { return
 template <typename T, class Op> __host__ __device__ constexpr bool compact_headline() {
   return sizeof(T) == 4 && Op::IN == 4;
 }
+// The other instantiations, (compute warps, sub-tiles per tile, staged tiles), measured at
+// 1e8 segments (scripts/kernel_probe.py): fp32 3D 12 x 24 x 3 (1.18 ms vs 1.40 at 16 x 16 x 3),
+// fp64 2D 8 x 16 x 2 (2.03 ms vs 2.27 at 8 x 8 x 3); homogeneous fp32 8 x 16 x 3 (1.83 ms,
+// better than 12 x 24 or 16 x 16, which spill).
+#ifndef CLIPSEG_F32_3D_W
+#define CLIPSEG_F32_3D_W 12
+#endif
+#ifndef CLIPSEG_F32_3D_N
+#define CLIPSEG_F32_3D_N 24
+#endif
+#ifndef CLIPSEG_F32_3D_B
+#define CLIPSEG_F32_3D_B 3
+#endif
+#ifndef CLIPSEG_F64_2D_W
+#define CLIPSEG_F64_2D_W 8
+#endif
+#ifndef CLIPSEG_F64_2D_N
+#define CLIPSEG_F64_2D_N 16
+#endif
+#ifndef CLIPSEG_F64_2D_B
+#define CLIPSEG_F64_2D_B 2
+#endif
+#ifndef CLIPSEG_F64_3D_W
+#define CLIPSEG_F64_3D_W 8
+#endif
+#ifndef CLIPSEG_F64_3D_N
+#define CLIPSEG_F64_3D_N 8
+#endif
+#ifndef CLIPSEG_F64_3D_B
+#define CLIPSEG_F64_3D_B 2
+#endif
+#ifndef CLIPSEG_F32_H_W
+#define CLIPSEG_F32_H_W 8
+#endif
+#ifndef CLIPSEG_F32_H_N
+#define CLIPSEG_F32_H_N 16
+#endif
+#ifndef CLIPSEG_F32_H_B
+#define CLIPSEG_F32_H_B 3
+#endif
+#ifndef CLIPSEG_F64_H_W
+#define CLIPSEG_F64_H_W 4
+#endif
+#ifndef CLIPSEG_F64_H_N
+#define CLIPSEG_F64_H_N 8
+#endif
+#ifndef CLIPSEG_F64_H_B
+#define CLIPSEG_F64_H_B 3
+#endif
+struct CompactKnobs {
+  int warps, nsub, nbuf;
+};
+template <typename T, class Op> __host__ __device__ constexpr CompactKnobs compact_knobs() {
+  return compact_headline<T, Op>() ? CompactKnobs{CLIPSEG_COMPUTE_WARPS, CLIPSEG_NSUB_F32_2D, CLIPSEG_NBUF_F32_2D}
+         : Op::IN == 8 ? (sizeof(T) == 4 ? CompactKnobs{CLIPSEG_F32_H_W, CLIPSEG_F32_H_N, CLIPSEG_F32_H_B}
+                                         : CompactKnobs{CLIPSEG_F64_H_W, CLIPSEG_F64_H_N, CLIPSEG_F64_H_B})
+         : Op::IN == 6 ? (sizeof(T) == 4 ? CompactKnobs{CLIPSEG_F32_3D_W, CLIPSEG_F32_3D_N, CLIPSEG_F32_3D_B}
+                                         : CompactKnobs{CLIPSEG_F64_3D_W, CLIPSEG_F64_3D_N, CLIPSEG_F64_3D_B})
+                       : CompactKnobs{CLIPSEG_F64_2D_W, CLIPSEG_F64_2D_N, CLIPSEG_F64_2D_B};
+}
 template <typename T, class Op> __host__ __device__ constexpr int compact_warps() {
-  return compact_headline<T, Op>() ? CLIPSEG_COMPUTE_WARPS
-                                   : (Op::IN == 8 ? (sizeof(T) == 4 ? 8 : 4) : (sizeof(T) == 4 ? 16 : 8));
+  return compact_knobs<T, Op>().warps;
 }
 template <typename T, class Op> __host__ __device__ constexpr int compact_subtiles() {
-  return compact_headline<T, Op>() ? CLIPSEG_NSUB_F32_2D : (sizeof(T) == 4 ? 16 : 8);
+  return compact_knobs<T, Op>().nsub;
 }
 template <typename T, class Op> __host__ __device__ constexpr int compact_buffers() {
-  return compact_headline<T, Op>() ? CLIPSEG_NBUF_F32_2D : ((sizeof(T) == 8 && Op::IN == 6) ? 2 : 3);
+  return compact_knobs<T, Op>().nbuf;
 }
 template <typename T, class Op> __host__ __device__ constexpr int compact_min_blocks() {
   return compact_headline<T, Op>() ? CLIPSEG_MINB_F32_2D : 1;

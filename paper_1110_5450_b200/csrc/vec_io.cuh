@@ -19,10 +19,23 @@ template <> struct Vec16<double> {
   static __device__ __forceinline__ double2 pack(const double (&a)[2]) { return make_double2(a[0], a[1]); }
 };
 
+#ifndef CLIPSEG_LOAD_HINT
+#define CLIPSEG_LOAD_HINT 0  // 0 evict-first (ld.cs), 1 ld.global.nc, 2 plain, 3 last-use (ld.lu)
+#endif
 // Evict-first streaming: every byte is touched exactly once per launch.
 template <typename T>
 __device__ __forceinline__ void load_vec(const T* p, T (&a)[Vec16<T>::N]) {
-  Vec16<T>::unpack(__ldcs(reinterpret_cast<const typename Vec16<T>::type*>(p)), a);
+  typedef typename Vec16<T>::type V;
+  const V* q = reinterpret_cast<const V*>(p);
+#if CLIPSEG_LOAD_HINT == 1
+  Vec16<T>::unpack(__ldg(q), a);
+#elif CLIPSEG_LOAD_HINT == 2
+  Vec16<T>::unpack(*q, a);
+#elif CLIPSEG_LOAD_HINT == 3
+  Vec16<T>::unpack(__ldlu(q), a);
+#else
+  Vec16<T>::unpack(__ldcs(q), a);
+#endif
 }
 template <typename T>
 __device__ __forceinline__ void store_vec(T* p, const T (&a)[Vec16<T>::N]) {
