@@ -62,17 +62,67 @@ MUTANTS = [
      "        if (0) {\n          Q1[k] = -qw1;", "killed"),
 ]
 
+# NEXT-2 / NEXT-3 oracles (Python): mutated in a temporary copy of the repository
+MUTANTS += [
+    ("M0 unmutated (harness check)", "tof_oracle.py", "import numpy as np", "import numpy as np", "equivalent"),
+    ("M0 unmutated (harness check)", "cluster_oracle.py", "import numpy as np", "import numpy as np", "equivalent"),
+    ("T1 open interval", "tof_oracle.py", "below = d < r_min", "below = d <= r_min", "killed"),
+    ("T2 sqrt dropped", "tof_oracle.py", "np.asarray(d, np.float64) * np.sqrt(np.asarray(I, np.float64))",
+     "np.asarray(d, np.float64) * np.asarray(I, np.float64)", "killed"),
+    ("T3 d = 0 accepted", "tof_oracle.py", "invalid = ~(d > 0)", "invalid = ~(d >= 0)", "killed"),
+    ("T4 I < 0 accepted", "tof_oracle.py", "| ~(I >= 0)", "| ~(I >= -1)", "killed"),
+    ("T5 wrong frame of a pixel", "tof_oracle.py", "f = np.arange(n, dtype=np.int64) // ppf",
+     "f = (np.arange(n, dtype=np.int64) + 1) // ppf", "killed"),
+    ("K1 ties to the smaller id", "cluster_oracle.py", "(d == bd and s > best)", "(d == bd and s < best)",
+     "killed"),
+    ("K2 merges need not be mutual", "cluster_oracle.py", "and r < s and best.get(s) == r]",
+     "and r < s and best.get(s) is not None]", "killed"),
+    ("K3 unweighted mean", "cluster_oracle.py", "regions[s] = [cs + cr, zs + zr, ps + pr]",
+     "regions[s] = [cs + cr, (zs / cs + zr / cr) / 2 * (cs + cr), (ps / cs + pr / cr) / 2 * (cs + cr)]", "killed"),
+    ("K4 strict Eq. (1)", "cluster_oracle.py", "abs(mr[0] - ms[0]) <= p[\"t_z\"]", "abs(mr[0] - ms[0]) < p[\"t_z\"]",
+     "killed"),
+    ("K5 Eq. (2) without phi", "cluster_oracle.py", " + p[\"alpha_phi\"] * abs(mr[1] - ms[1])", "", "killed"),
+    ("K6 survivor keeps the smaller id", "cluster_oracle.py",
+     "pairs = [(r, s) for r, s in best.items() if s is not None and r < s and best.get(s) == r]",
+     "pairs = [(s, r) for r, s in best.items() if s is not None and r < s and best.get(s) == r]", "killed"),
+]
+
 TESTS = {"clip_oracle_impl.h": ["tests/test_oracle_pins.py", "tests/test_oracle_homog.py"],
-         "clip_homog_impl.h": ["tests/test_oracle_homog.py"]}
+         "clip_homog_impl.h": ["tests/test_oracle_homog.py"],
+         "tof_oracle.py": ["tests/test_oracle_tof.py"],
+         "cluster_oracle.py": ["tests/test_oracle_cluster.py"]}
+
+
+def run_python_mutant(fname, orig, mut):
+    """Mutate a Python oracle in a temporary copy of the repository and run its pins there."""
+    with tempfile.TemporaryDirectory() as td:
+        repo = os.path.join(td, "repo")
+        shutil.copytree(ROOT, repo, ignore=shutil.ignore_patterns(".git", "build", "gpurun_out", "__pycache__",
+                                                                  ".pytest_cache", "profiles"))
+        path = os.path.join(repo, "oracle", fname)
+        text = open(path).read()
+        assert text.count(orig) >= 1, (fname, orig)
+        open(path, "w").write(text.replace(orig, mut, 1))
+        r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-m", "not gpu", "-p", "no:cacheprovider",
+                            *TESTS[fname]], cwd=repo, capture_output=True, text=True)
+        return r.returncode != 0
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", choices=["cuboid", "homog"])
+    ap.add_argument("--only", choices=["cuboid", "homog", "python"])
     a = ap.parse_args()
     rows, bad = [], 0
     for mid, fname, orig, mut, expect in MUTANTS:
-        if a.only == "cuboid" and fname != "clip_oracle_impl.h" or a.only == "homog" and fname != "clip_homog_impl.h":
+        if (a.only == "cuboid" and fname != "clip_oracle_impl.h" or a.only == "homog" and fname != "clip_homog_impl.h"
+                or a.only == "python" and not fname.endswith(".py")):
+            continue
+        if fname.endswith(".py"):
+            got = "killed" if run_python_mutant(fname, orig, mut) else "survived"
+            ok = (got == "killed") == (expect == "killed")
+            bad += not ok
+            rows.append((mid, got, expect, "ok" if ok else "UNEXPECTED"))
+            print(f"{mid:30s} {got:9s} (expected {expect}) {'' if ok else '<-- UNEXPECTED'}", flush=True)
             continue
         with tempfile.TemporaryDirectory() as td:
             src = os.path.join(td, "oracle")

@@ -124,3 +124,57 @@ def test_properties_on_scenes(seed):
     for r in reg:
         zz = z[lab == r]
         assert zz.max() - zz.min() < 1.0
+
+
+def test_waiting_region_and_closed_threshold():
+    """Rule 3 (Fig. 3 caption "have to wait"): values (0, 10, 12), t = 40: best(1) = 2
+    but best(2) = 3, so only {2, 3} merges in round 1 (id 3, value 11) and region 1 waits;
+    round 2 merges {1, 3} (value 22/3).  Eq. (1) is the closed |dw| <= t: a
+    difference of exactly t merges, one just above it does not."""
+    p = dict(t_z=1.0, t_phi=40.0, alpha_z=0.0, alpha_phi=1.0)
+    pp = dict(P, **p)
+    regions, nbrs = C.init_regions(np.zeros((1, 3), np.float32), np.array([[0, 10, 12]], np.float32),
+                                   np.ones((1, 3), bool))
+    assert C.merge_round(regions, nbrs, pp) == 1
+    assert sorted(regions) == [1, 3] and C.mean(regions[3])[1] == 11 and C.mean(regions[1])[1] == 0
+    assert C.merge_round(regions, nbrs, pp) == 1 and sorted(regions) == [3]
+    assert C.mean(regions[3])[1] == 22 / 3
+    z = np.zeros((1, 2), np.float32)
+    lab, reg, _, _ = C.cluster(z, np.array([[0, 40]], np.float32), np.ones((1, 2), bool), p)
+    assert len(reg) == 1
+    lab, reg, _, _ = C.cluster(z, np.array([[0, np.nextafter(np.float32(40), np.float32(50))]], np.float32),
+                               np.ones((1, 2), bool), p)
+    assert len(reg) == 2
+    pz = dict(t_z=1.0, t_phi=1.0, alpha_z=1.0, alpha_phi=0.0)     # the same on the z component
+    lab, reg, _, _ = C.cluster(np.array([[0, 1]], np.float32), np.zeros((1, 2), np.float32), np.ones((1, 2), bool),
+                               pz)
+    assert len(reg) == 1
+
+
+@pytest.mark.parametrize("seed", [4, 5])
+def test_round_is_the_mutual_best_matching(seed):
+    """Every round, checked from a snapshot of the frozen state with an independent argmin
+    (sorted by (distance, -id)): the merged pairs are exactly the mutual best choices, each
+    region is in at most one pair, and the survivor is the larger id with summed count/sums."""
+    import copy
+    z, ph, v, _ = scenes.scene(24, 24, seed)
+    regions, nbrs = C.init_regions(z, ph, v)
+    for _ in range(60):
+        before_r, before_n = copy.deepcopy(regions), copy.deepcopy(nbrs)
+        means = {r: (x[1] / x[0], x[2] / x[0]) for r, x in before_r.items()}
+        choice = {}
+        for r, ns in before_n.items():
+            ok = [s for s in ns if abs(means[r][0] - means[s][0]) <= P["t_z"]
+                  and abs(means[r][1] - means[s][1]) <= P["t_phi"]]
+            key = lambda s, r=r: (P["alpha_z"] * abs(means[r][0] - means[s][0])  # noqa: E731
+                                  + P["alpha_phi"] * abs(means[r][1] - means[s][1]), -s)
+            choice[r] = sorted(ok, key=key)[0] if ok else None
+        want = {(min(r, s), max(r, s)) for r, s in choice.items() if s is not None and choice[s] == r}
+        k = C.merge_round(regions, nbrs, P)
+        assert k == len(want)
+        assert set(before_r) - set(regions) == {a for a, b in want}
+        for a, b in want:
+            assert regions[b] == [before_r[a][0] + before_r[b][0], before_r[a][1] + before_r[b][1],
+                                  before_r[a][2] + before_r[b][2]]
+        if k == 0:
+            break
