@@ -9,10 +9,12 @@
 //    prefixes (flag P).  A tile's offset is thus known about one L2 round trip after the
 //    last of its predecessors has published, with no redundant per-tile walks;
 //
-//  * every other block claims block tiles of BT = NSUB x 128 segments in increasing order
-//    from an atomic counter (the first of its compute warps to start a tile claims the
-//    block's next one, so claims follow the order blocks start computing) and runs
-//      - 8 compute warps.  Per sub-tile (32 lanes x 4 segments, one 128-bit load per plane
+//  * every other block (one per SM) claims block tiles of BT = NSUB x 128 segments in
+//    increasing order from an atomic counter (the first of its compute warps to start a
+//    tile claims the block's next one, so claims follow the order blocks start computing;
+//    the shapes per instantiation are in clip_kernels.cuh — fp32 2D: 16 compute warps, 32
+//    sub-tiles, 3 staged tiles) and runs
+//      - the compute warps.  Per sub-tile (32 lanes x 4 segments, one 128-bit load per plane
 //        per lane; the next sub-tile's loads — across tile boundaries — in flight while this
 //        one is clipped) a warp
 //        classifies and clips its segments (clip_math.cuh), stores the flags, warp-scans the
@@ -24,9 +26,9 @@
 //      - 1 scan warp: once tile k's counts are in, it prefix-sums the NSUB sub-tile counts,
 //        waits for the scanner's inclusive prefix of the tile and hands the offsets over.
 //
-// Hand-offs inside a block use shared-memory mbarriers (compute warps -> scan warp: 8
-// arrivals per tile; scan warp -> compute warps: 1; claiming warp -> all: the tile id, a
-// ring of 8).  Status words are 64-bit: flag in bits 62-63 (0 not ready, 1 aggregate,
+// Hand-offs inside a block use shared-memory mbarriers (compute warps -> scan warp: one
+// arrival per compute warp per tile; scan warp -> compute warps: 1; claiming warp -> all:
+// the tile id, a ring of 8).  Status words are 64-bit: flag in bits 62-63 (0 not ready, 1 aggregate,
 // 2 inclusive prefix), value in bits 0-61.  The scanner writes the total count.
 #include <type_traits>
 
