@@ -224,3 +224,37 @@ def test_sharded_compact_single_rank_nccl(torch, cs):
         assert np.array_equal(b.index.cpu().numpy()[:wcnt], widx)
     finally:
         dist.destroy_process_group()
+
+
+def test_negative_zero_window_takes_the_exact_path(torch, cs):
+    """A -0 window edge disables the fast path (clip_math.cuh): every group runs the rules
+    select by select; results stay bit-identical (signed zeros included)."""
+    n = 100003
+    planes, _ = gen(synth.ADVERSARIAL, 2, synth.seed_for(3, 7), n, np.float32)
+    lo, hi = [-0.0, 0.0], [1.0, 1.0]
+    check_dense(torch, cs, planes, n, lo, hi, 2)
+    check_compact(torch, cs, planes, n, lo, hi, 2)
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_padded_strides(torch, cs, dtype):
+    """Input and output planes with different, padded strides (ld > n, ld_in != ld_out; the ABI
+    requires 16-byte aligned planes, checked in test_abi)."""
+    n = 50007
+    planes, _ = gen(synth.MIX, 3, synth.seed_for(2, 8), n, dtype)
+    want, wflags = oracle.clip(planes, n, *UNIT[3], 3)
+    wc, widx, wcnt, wcf = oracle.compact(planes, n, *UNIT[3], 3, with_flags=True)
+    tdt = torch.float32 if dtype == np.float32 else torch.float64
+    ld = synth.plane_stride(n)
+    d_in = torch.zeros((6, ld + 96), dtype=tdt, device="cuda")
+    d_in[:, :n] = torch.from_numpy(planes[:, :n]).cuda()
+    out = torch.zeros((6, ld + 160), dtype=tdt, device="cuda")
+    out, flags = cs.clip(d_in, n, *UNIT[3], out=out)
+    b = cs.CompactBuffers(n, 3, tdt, with_flags=True, with_index=True)
+    b.out = torch.zeros((6, ld + 224), dtype=tdt, device="cuda")
+    cs.clip_compact(d_in, n, *UNIT[3], bufs=b)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(out.cpu().numpy()[:, :n]), bits(want[:, :n]))
+    assert int(b.count.item()) == wcnt
+    assert np.array_equal(bits(b.out.cpu().numpy()[:, :wcnt]), bits(wc[:, :wcnt]))
+    assert np.array_equal(b.index.cpu().numpy()[:wcnt], widx)
