@@ -250,7 +250,10 @@ cudaError_t launch_cluster(const float* z, const float* phi, const uint8_t* vali
     const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, cluster_kernel, 256, 0);
     if (e != cudaSuccess || blocks_per_sm < 1) blocks_per_sm = 1;
   }
-  const int64_t want = (2 * n + 255) / 256;
+#ifndef CLIPSEG_CLUSTER_PIX_PER_BLOCK
+#define CLIPSEG_CLUSTER_PIX_PER_BLOCK 512  // pixels per block (128..2048 measured alike; 8192 slower)
+#endif
+  const int64_t want = (n + CLIPSEG_CLUSTER_PIX_PER_BLOCK - 1) / CLIPSEG_CLUSTER_PIX_PER_BLOCK;
   const int64_t cap = (int64_t)device_sm_count() * blocks_per_sm;
   const int grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
   void* args[] = {(void*)&z, (void*)&phi, (void*)&valid, (void*)&nframes, (void*)&H, (void*)&W, (void*)&prm,
