@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(CompactShape<T, Op, INDEX>::kThreads, CompactS
       const int o = (32 * j + lane) * V;
       if (FULL || o < rem) {
 #pragma unroll
-        for (int c = 0; c < IN; ++c) load_vec<T>(src + c * ld_in + o, dst[j][c]);
+        for (int c = 0; c < IN; ++c) load_vec<T, IN == 4>(src + c * ld_in + o, dst[j][c]);
       } else {
 #pragma unroll
         for (int c = 0; c < IN; ++c)

@@ -23,7 +23,7 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 3 : 2)
   T nxt[IN][V];
   if (g < ngroups) {
 #pragma unroll
-    for (int c = 0; c < IN; ++c) load_vec<T>(in + c * ld_in + g * V, nxt[c]);
+    for (int c = 0; c < IN; ++c) load_vec<T, IN == 4>(in + c * ld_in + g * V, nxt[c]);
   }
   for (; g < ngroups; g += stride) {
     const int64_t i = g * V;
@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(256, sizeof(T) == 4 ? 3 : 2)
       for (int v = 0; v < V; ++v) plane[c][v] = nxt[c][v];
     if (g + stride < ngroups) {  // next group's loads in flight while this one is clipped
 #pragma unroll
-      for (int c = 0; c < IN; ++c) load_vec<T>(in + c * ld_in + (g + stride) * V, nxt[c]);
+      for (int c = 0; c < IN; ++c) load_vec<T, IN == 4>(in + c * ld_in + (g + stride) * V, nxt[c]);
     }
     T res[OUT][V];
     const unsigned bits = Op::template group<V, true>(plane, w, res);

@@ -20,22 +20,28 @@ template <> struct Vec16<double> {
 };
 
 #ifndef CLIPSEG_LOAD_HINT
-#define CLIPSEG_LOAD_HINT 0  // 0 evict-first (ld.cs), 1 ld.global.nc, 2 plain, 3 last-use (ld.lu)
+#define CLIPSEG_LOAD_HINT 2  // streaming loads of 2D segments: 0 evict-first, 1 .nc, 2 plain, 3 last-use
 #endif
-// Evict-first streaming: every byte is touched exactly once per launch.
-template <typename T>
+// Streaming loads (every byte is read once per launch).  PLAIN selects plain loads, measured
+// ~2-7 % faster than evict-first ones for the 2D fp32 kernels (dense 0.617 -> 0.575 ms at 1e8)
+// and slower for the 3D / homogeneous ones, which keep evict-first (profiles/r01_summary.md).
+template <typename T, bool PLAIN = false>
 __device__ __forceinline__ void load_vec(const T* p, T (&a)[Vec16<T>::N]) {
   typedef typename Vec16<T>::type V;
   const V* q = reinterpret_cast<const V*>(p);
+  if (PLAIN) {
 #if CLIPSEG_LOAD_HINT == 1
-  Vec16<T>::unpack(__ldg(q), a);
+    Vec16<T>::unpack(__ldg(q), a);
 #elif CLIPSEG_LOAD_HINT == 2
-  Vec16<T>::unpack(*q, a);
+    Vec16<T>::unpack(*q, a);
 #elif CLIPSEG_LOAD_HINT == 3
-  Vec16<T>::unpack(__ldlu(q), a);
+    Vec16<T>::unpack(__ldlu(q), a);
 #else
-  Vec16<T>::unpack(__ldcs(q), a);
+    Vec16<T>::unpack(__ldcs(q), a);
 #endif
+  } else {
+    Vec16<T>::unpack(__ldcs(q), a);
+  }
 }
 template <typename T>
 __device__ __forceinline__ void store_vec(T* p, const T (&a)[Vec16<T>::N]) {
