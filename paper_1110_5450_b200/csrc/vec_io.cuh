@@ -45,7 +45,11 @@ __device__ __forceinline__ void load_vec(const T* p, T (&a)[Vec16<T>::N]) {
 }
 template <typename T>
 __device__ __forceinline__ void store_vec(T* p, const T (&a)[Vec16<T>::N]) {
+#if defined(CLIPSEG_PLAIN_STORES)
+  *reinterpret_cast<typename Vec16<T>::type*>(p) = Vec16<T>::pack(a);
+#else
   __stcs(reinterpret_cast<typename Vec16<T>::type*>(p), Vec16<T>::pack(a));
+#endif
 }
 
 }  // namespace clipseg
