@@ -35,14 +35,14 @@ struct ClusterWs {  // views into the caller's workspace, n = nframes * P region
   int* parent;                  // g, or the region that absorbed g
   int* bestid[2];               // rule 2 choice (partner id, 0 = none), per round parity
   unsigned long long* bestd[2]; // minimum Eq. (2) distance (bits of a non-negative double)
+  unsigned long long* ed;       // this round's live edges: Eq. (2) distance bits, ~0 if not allowed
   int* ea[2];                   // live edge lists (endpoints), per round parity
   int* eb[2];
   int* rl[2];                   // live region lists, per round parity
   int* counts;                  // [0..1] live edges, [2..3] live regions, [4..5] merges, [6] flag
   double* sz;                   // fp64 sums of the pixels' binary32 z and phi (DESIGN M-b)
   double* sp;
-  double* mz;                   // means sz / cnt, sp / cnt
-  double* mp;
+  double2* m;                   // means (sz / cnt, sp / cnt): one 16-byte load per endpoint
 };
 
 struct MergeParams {
@@ -50,7 +50,8 @@ struct MergeParams {
 };
 
 __device__ __forceinline__ bool eq1(const ClusterWs& w, int a, int b, const MergeParams& p, double* dist) {
-  const double dz = fabs(__dsub_rn(w.mz[a], w.mz[b])), dp = fabs(__dsub_rn(w.mp[a], w.mp[b]));
+  const double2 ma = w.m[a], mb = w.m[b];
+  const double dz = fabs(__dsub_rn(ma.x, mb.x)), dp = fabs(__dsub_rn(ma.y, mb.y));
   *dist = __dadd_rn(__dmul_rn(p.alpha_z, dz), __dmul_rn(p.alpha_phi, dp));  // Eq. (2)
   return dz <= p.t_z && dp <= p.t_phi;                                         // Eq. (1)
 }
@@ -90,8 +91,7 @@ __global__ void __launch_bounds__(256) cluster_kernel(const float* __restrict__ 
     const double zz = v ? (double)z[g] : 0.0, pp = v ? (double)phi[g] : 0.0;
     w.sz[g] = zz;
     w.sp[g] = pp;
-    w.mz[g] = zz;
-    w.mp[g] = pp;
+    w.m[g] = make_double2(zz, pp);
     const int64_t q = g % P;
     const int x = (int)(q % W), y = (int)(q / W);
     const bool r = v && x + 1 < W && valid[g + 1] != 0, d = v && y + 1 < H && valid[g + W] != 0;
@@ -124,8 +124,10 @@ __global__ void __launch_bounds__(256) cluster_kernel(const float* __restrict__ 
       w.ea[nxt][slot] = a;
       w.eb[nxt][slot] = b;
       double dist;
-      if (eq1(w, a, b, prm, &dist)) {
-        const unsigned long long bits = (unsigned long long)__double_as_longlong(dist);
+      const bool ok = eq1(w, a, b, prm, &dist);
+      const unsigned long long bits = ok ? (unsigned long long)__double_as_longlong(dist) : ~0ull;
+      w.ed[slot] = bits;  // phase B reads it back instead of recomputing from random means
+      if (ok) {
         atomicMin(w.bestd[cur] + a, bits);
         atomicMin(w.bestd[cur] + b, bits);
       }
@@ -135,13 +137,11 @@ __global__ void __launch_bounds__(256) cluster_kernel(const float* __restrict__ 
     const int ne2 = ecount[nxt];
     if (t0 == 0) ecount[cur] = 0;  // the list just read becomes the next round's output
     for (int64_t e = t0; e < ne2; e += stride) {
+      const unsigned long long bits = w.ed[e];
+      if (bits == ~0ull) continue;  // not allowed by Eq. (1)
       const int a = w.ea[nxt][e], b = w.eb[nxt][e];
-      double dist;
-      if (eq1(w, a, b, prm, &dist)) {
-        const unsigned long long bits = (unsigned long long)__double_as_longlong(dist);
-        if (bits == w.bestd[cur][a]) atomicMax(w.bestid[cur] + a, (int)(b % P) + 1);
-        if (bits == w.bestd[cur][b]) atomicMax(w.bestid[cur] + b, (int)(a % P) + 1);
-      }
+      if (bits == w.bestd[cur][a]) atomicMax(w.bestid[cur] + a, (int)(b % P) + 1);
+      if (bits == w.bestd[cur][b]) atomicMax(w.bestid[cur] + b, (int)(a % P) + 1);
     }
     grid.sync();
     // C: mutual pairs merge into the larger id (rule 3); the next live region list
@@ -163,8 +163,7 @@ __global__ void __launch_bounds__(256) cluster_kernel(const float* __restrict__ 
         w.cnt[g] = c;
         w.sz[g] = s1;
         w.sp[g] = s2;
-        w.mz[g] = __ddiv_rn(s1, (double)c);
-        w.mp[g] = __ddiv_rn(s2, (double)c);
+        w.m[g] = make_double2(__ddiv_rn(s1, (double)c), __ddiv_rn(s2, (double)c));
         atomicAdd(merges + cur, 1);
       }
       const int slot = append_slot(rcount + nxt, !absorbed);
@@ -207,8 +206,9 @@ __global__ void __launch_bounds__(256) cluster_kernel(const float* __restrict__ 
 }  // namespace
 
 size_t cluster_workspace_bytes(int64_t n) {
-  // sums/means 4 x 8, choices 2 x (8 + 4), cnt/parent 2 x 4, edges 2 x 2 x 2 x 4, regions 2 x 4
-  return (size_t)n * (32 + 24 + 8 + 32 + 8) + 16 * 256;
+  // sums/means 4 x 8, choices 2 x (8 + 4), cnt/parent 2 x 4, edges 2 x 2 x 2 x 4, edge
+  // distances 2 x 8, regions 2 x 4
+  return (size_t)n * (32 + 24 + 8 + 32 + 16 + 8) + 16 * 256;
 }
 
 cudaError_t launch_cluster(const float* z, const float* phi, const uint8_t* valid, int64_t nframes, int H, int W,
@@ -224,8 +224,7 @@ cudaError_t launch_cluster(const float* z, const float* phi, const uint8_t* vali
   };
   w.sz = reinterpret_cast<double*>(take(8 * n));
   w.sp = reinterpret_cast<double*>(take(8 * n));
-  w.mz = reinterpret_cast<double*>(take(8 * n));
-  w.mp = reinterpret_cast<double*>(take(8 * n));
+  w.m = reinterpret_cast<double2*>(take(16 * n));
   for (int q = 0; q < 2; ++q) {
     w.bestd[q] = reinterpret_cast<unsigned long long*>(take(8 * n));
     w.bestid[q] = reinterpret_cast<int*>(take(4 * n));
@@ -233,6 +232,7 @@ cudaError_t launch_cluster(const float* z, const float* phi, const uint8_t* vali
     w.eb[q] = reinterpret_cast<int*>(take(8 * n));
     w.rl[q] = reinterpret_cast<int*>(take(4 * n));
   }
+  w.ed = reinterpret_cast<unsigned long long*>(take(16 * n));
   w.cnt = reinterpret_cast<int*>(take(4 * n));
   w.parent = reinterpret_cast<int*>(take(4 * n));
   w.counts = reinterpret_cast<int*>(take(64));
