@@ -33,7 +33,6 @@ template <typename T, bool NDC> struct HomogOp {  // NEXT-1: homogeneous clip sp
 
 // Workspace of the compacting kernel: a 128-byte header (tile-claim counter) followed by
 // one 64-bit look-back status word per tile.
-constexpr int kCompactThreads = 256;
 constexpr size_t kWsHeaderBytes = 128;
 
 template <typename T> __host__ __device__ constexpr int vec_elems() { return 16 / (int)sizeof(T); }
