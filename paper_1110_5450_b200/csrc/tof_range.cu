@@ -3,10 +3,8 @@
 // recomputed per frame) as a 2-bit outcode, fused with phi = arctan(d sqrt(I)) of Eq. (5)
 // for the kept pixels, plus the kept-pixel count per frame.
 //
-// HBM-bound map: 8 bytes in (d, I) and 5 out (phi, code) per pixel.  One thread owns 4
-// consecutive pixels (128-bit loads / stores, evict-first); a warp owns 128 consecutive
-// pixels, so with frames of >= 128 pixels (the paper's are 204^2) its pixels span at most
-// two frames and the per-frame counts are two warp reductions and <= 2 atomics per warp.
+// HBM-bound map: 8 bytes in (d, I) and 5 out (phi, code) per pixel, 128-bit evict-first
+// loads and stores; the per-frame counts are one warp reduction and one atomic per chunk.
 #include <cuda_runtime.h>
 
 #include <cfloat>
@@ -62,92 +60,81 @@ __device__ __forceinline__ float tof_phi(float d, float I) {
   return big ? __fsub_rn(1.5707963267948966f, a) : a;
 }
 
-template <bool COUNT_WARP>
+// A warp owns chunks of kChunk = 32 lanes x kG vectors x 4 pixels; lane l loads vector
+// (32 j + l) of the chunk for j < kG, so each 128-bit load instruction is fully coalesced and
+// every lane has kG x 8 loads in flight.  A chunk inside one frame (the common case: frames
+// are 41616 pixels) costs one frame lookup, one range load, one warp reduction and at most
+// one atomic; chunks straddling a frame boundary or the end take a per-pixel path.
+constexpr int kG = 4;
+constexpr int64_t kChunk = 32 * kG * 4;
+
 __global__ void __launch_bounds__(256) tof_range_phi_kernel(const float* __restrict__ d, const float* __restrict__ I,
                                                             int64_t n, int64_t ppf, const float* __restrict__ ranges,
                                                             float* __restrict__ phi, uint8_t* __restrict__ code,
                                                             int* __restrict__ kept, double inv_ppf) {
   const int lane = threadIdx.x & 31;
-  const int64_t ngroups = (n + 3) / 4;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  float4 nd = make_float4(0.f, 0.f, 0.f, 0.f), nI = nd;
-  auto load = [&](int64_t gg, float4& a, float4& b) {  // group gg's 4 pixels (0 past the end)
-    const int64_t i = gg * 4;
-    if (i + 4 <= n) {
-      a = __ldcs(reinterpret_cast<const float4*>(d + i));
-      b = __ldcs(reinterpret_cast<const float4*>(I + i));
-    } else {
-      a = make_float4(i < n ? d[i] : 0.f, i + 1 < n ? d[i + 1] : 0.f, i + 2 < n ? d[i + 2] : 0.f, 0.f);
-      b = make_float4(i < n ? I[i] : 0.f, i + 1 < n ? I[i + 1] : 0.f, i + 2 < n ? I[i + 2] : 0.f, 0.f);
-    }
-  };
-  if (g < ngroups) load(g, nd, nI);
-  // whole warps iterate together (the warp reductions need every lane)
-  for (; g - lane < ngroups; g += stride) {
-    const float dv[4] = {nd.x, nd.y, nd.z, nd.w}, Iv[4] = {nI.x, nI.y, nI.z, nI.w};
-    if (g + stride < ngroups) load(g + stride, nd, nI);  // next group's loads in flight
-    const int64_t i0 = g * 4;
-    const bool live = g < ngroups;
-    const int64_t f0 = frame_of(live ? i0 : 0, ppf, inv_ppf);
-    const float lo0 = __ldg(ranges + 2 * f0), hi0 = __ldg(ranges + 2 * f0 + 1);
-    float pv[4];
-    uint32_t cpack = 0;
-    int cnt_lo = 0, cnt_hi = 0;  // kept pixels in frame f0 / in later frames
-    if (live && i0 + 4 <= n && i0 + 3 - f0 * ppf < ppf) {  // the common case: 4 pixels of frame f0
+  const int64_t warp_id = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t nchunks = (n + kChunk - 1) / kChunk;
+  for (int64_t ch = warp_id; ch < nchunks; ch += nwarps) {
+    const int64_t p0 = ch * kChunk;
+    const bool full = p0 + kChunk <= n;
+    float dv[kG][4], Iv[kG][4];
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const uint32_t c = tof_code(dv[v], Iv[v], lo0, hi0);
-        const float ph = tof_phi(dv[v], Iv[v]);
-        pv[v] = c == 0u ? ph : __int_as_float(0x7FC00000);
-        cpack |= c << (8 * v);
-        cnt_lo += c == 0u;
-      }
-    } else {  // the group crosses a frame boundary or the end
+    for (int j = 0; j < kG; ++j) {
+      const int64_t i = p0 + (int64_t)(32 * j + lane) * 4;
+      if (full) {
+        const float4 a = __ldcs(reinterpret_cast<const float4*>(d + i));
+        const float4 b = __ldcs(reinterpret_cast<const float4*>(I + i));
+        dv[j][0] = a.x; dv[j][1] = a.y; dv[j][2] = a.z; dv[j][3] = a.w;
+        Iv[j][0] = b.x; Iv[j][1] = b.y; Iv[j][2] = b.z; Iv[j][3] = b.w;
+      } else {
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const bool valid = live && i0 + v < n;
-        const int64_t f = valid ? frame_of(i0 + v, ppf, inv_ppf) : f0;
-        const float lo = __ldg(ranges + 2 * f), hi = __ldg(ranges + 2 * f + 1);
-        const uint32_t c = tof_code(dv[v], Iv[v], lo, hi);
-        const bool keep = valid && c == 0u;
-        pv[v] = keep ? tof_phi(dv[v], Iv[v]) : __int_as_float(0x7FC00000);
-        cpack |= c << (8 * v);
-        if (keep) {
-          if (COUNT_WARP) {
-            if (f == f0) ++cnt_lo; else ++cnt_hi;
-          } else if (kept) {
-            atomicAdd(kept + f, 1);
-          }
+        for (int v = 0; v < 4; ++v) {
+          dv[j][v] = i + v < n ? d[i + v] : 0.0f;
+          Iv[j][v] = i + v < n ? I[i + v] : 0.0f;
         }
       }
-      if (!COUNT_WARP) cnt_lo = 0;
     }
-    if (live) {
-      if (i0 + 4 <= n) {
-        __stcs(reinterpret_cast<float4*>(phi + i0), make_float4(pv[0], pv[1], pv[2], pv[3]));
-        if (code) __stcs(reinterpret_cast<unsigned int*>(code + i0), cpack);
-      } else {
-        for (int v = 0; v < 4; ++v)
-          if (i0 + v < n) {
-            phi[i0 + v] = pv[v];
-            if (code) code[i0 + v] = (uint8_t)(cpack >> (8 * v));
-          }
+    const int64_t last = (full ? p0 + kChunk : n) - 1;
+    const int64_t fa = frame_of(p0, ppf, inv_ppf), fb = frame_of(last, ppf, inv_ppf);
+    if (full && fa == fb) {  // warp-uniform: the whole chunk lies in frame fa
+      const float lo = __ldg(ranges + 2 * fa), hi = __ldg(ranges + 2 * fa + 1);
+      int cnt = 0;
+#pragma unroll
+      for (int j = 0; j < kG; ++j) {
+        const int64_t i = p0 + (int64_t)(32 * j + lane) * 4;
+        float pv[4];
+        uint32_t cpack = 0;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          const uint32_t c = tof_code(dv[j][v], Iv[j][v], lo, hi);
+          const float ph = tof_phi(dv[j][v], Iv[j][v]);
+          pv[v] = c == 0u ? ph : __int_as_float(0x7FC00000);
+          cpack |= c << (8 * v);
+          cnt += c == 0u;
+        }
+        __stcs(reinterpret_cast<float4*>(phi + i), make_float4(pv[0], pv[1], pv[2], pv[3]));
+        if (code) __stcs(reinterpret_cast<unsigned int*>(code + i), cpack);
       }
-    }
-    if (COUNT_WARP) {
-      // the warp's 128 pixels span frames fw and fw + 1 at most (ppf >= 128)
-      const int64_t fw = __shfl_sync(0xFFFFFFFFu, f0, 0);
-      const int lo_c = (f0 == fw) ? cnt_lo : 0;
-      const int hi_c = (f0 == fw) ? cnt_hi : cnt_lo + cnt_hi;
-      const int s_lo = __reduce_add_sync(0xFFFFFFFFu, lo_c);
-      const int s_hi = __reduce_add_sync(0xFFFFFFFFu, hi_c);
-      if (lane == 0) {
-        if (s_lo) atomicAdd(kept + fw, s_lo);
-        if (s_hi) atomicAdd(kept + fw + 1, s_hi);
+      if (kept) {
+        const int s = __reduce_add_sync(0xFFFFFFFFu, cnt);
+        if (lane == 0 && s) atomicAdd(kept + fa, s);
       }
-    } else if (kept && cnt_lo) {
-      atomicAdd(kept + f0, cnt_lo);  // the common-case group of the per-pixel-atomic variant
+    } else {  // a frame boundary or the end inside the chunk: pixel by pixel
+#pragma unroll
+      for (int j = 0; j < kG; ++j) {
+        const int64_t i = p0 + (int64_t)(32 * j + lane) * 4;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          if (i + v >= n) continue;
+          const int64_t f = frame_of(i + v, ppf, inv_ppf);
+          const uint32_t c = tof_code(dv[j][v], Iv[j][v], __ldg(ranges + 2 * f), __ldg(ranges + 2 * f + 1));
+          phi[i + v] = c == 0u ? tof_phi(dv[j][v], Iv[j][v]) : __int_as_float(0x7FC00000);
+          if (code) code[i + v] = (uint8_t)c;
+          if (kept && c == 0u) atomicAdd(kept + f, 1);
+        }
+      }
     }
   }
 }
@@ -162,20 +149,16 @@ cudaError_t launch_tof_range_phi(const float* d, const float* I, int64_t n, int6
     if (e != cudaSuccess) return e;
   }
   constexpr int NT = 256;
-  static int blocks_per_sm = 0;  // cached device attribute (both instantiations are alike)
+  static int blocks_per_sm = 0;  // cached device attribute
   if (!blocks_per_sm) {
-    const cudaError_t e =
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, tof_range_phi_kernel<true>, NT, 0);
+    const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, tof_range_phi_kernel, NT, 0);
     if (e != cudaSuccess || blocks_per_sm < 1) blocks_per_sm = 1;
   }
-  const int64_t ngroups = (n + 3) / 4;
-  const int64_t want = (ngroups + NT - 1) / NT;
+  const int64_t nchunks = (n + kChunk - 1) / kChunk;
+  const int64_t want = (nchunks * 32 + NT - 1) / NT;
   const int64_t cap = (int64_t)device_sm_count() * blocks_per_sm;  // persistent: one resident wave
   const int grid = (int)(want < cap ? want : cap);
-  if (kept && ppf >= 128)
-    tof_range_phi_kernel<true><<<grid, NT, 0, s>>>(d, I, n, ppf, ranges, phi, code, kept, 1.0 / (double)ppf);
-  else
-    tof_range_phi_kernel<false><<<grid, NT, 0, s>>>(d, I, n, ppf, ranges, phi, code, kept, 1.0 / (double)ppf);
+  tof_range_phi_kernel<<<grid, NT, 0, s>>>(d, I, n, ppf, ranges, phi, code, kept, 1.0 / (double)ppf);
   return cudaGetLastError();
 }
 
