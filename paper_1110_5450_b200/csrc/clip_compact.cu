@@ -209,6 +209,7 @@ template <typename T, class Op, bool INDEX> struct CompactShape {
   static constexpr size_t kSmemBytes = (size_t)NBUF * kBufBytes;
   static constexpr int kMinBlocks = compact_min_blocks<T, Op>();
   static constexpr int kComputeWarps = compact_warps<T, Op>();
+  static constexpr bool kPrefetch = compact_prefetch<T, Op>();
   static constexpr int kThreads = (kComputeWarps + 1) * 32;  // + the scan warp
 };
 
@@ -342,10 +343,13 @@ __global__ void __launch_bounds__(CompactShape<T, Op, INDEX>::kThreads, CompactS
   };
   // Sub-tile loads run one ahead of the clipping, across tile boundaries: the next tile is
   // claimed as this one starts, and its first sub-tile is loaded during this one's last.
-  T buf[2][IT][IN][V];
+  // PREFETCH: the next sub-tile's loads are in flight (in a second register buffer) while
+  // this one is clipped; without it (wide homogeneous rows) the registers go to more warps.
+  constexpr bool PREFETCH = S::kPrefetch;
+  T buf[PREFETCH ? 2 : 1][IT][IN][V];
   mbar_wait(&mb_tile[0], 0u);
   int64_t tile = s_tile[0];
-  if (tile < ntiles) load(tile, warp, buf[0], false);
+  if (PREFETCH && tile < ntiles) load(tile, warp, buf[0], false);
   for (int64_t k = 0;; ++k) {
     int64_t next = ntiles;
     if (tile < ntiles && lane == 0) {
@@ -372,25 +376,33 @@ __global__ void __launch_bounds__(CompactShape<T, Op, INDEX>::kThreads, CompactS
           // the other (static indices keep both in registers); with an odd one the current
           // sub-tile is copied out of buf[0] first.
           constexpr bool PING = (PER_WARP % 2) == 0;
-          const int cur = PING ? (r & 1) : 0;
           T held[IT][IN][V];
-          if (!PING) {
-#pragma unroll
-            for (int j = 0; j < IT; ++j)
-#pragma unroll
-              for (int c = 0; c < IN; ++c)
-#pragma unroll
-                for (int v = 0; v < V; ++v) held[j][c][v] = buf[0][j][c][v];
-          }
-          T (&dst)[IT][IN][V] = PING ? buf[cur ^ 1] : buf[0];
-          if (r + 1 < PER_WARP) {
-            load(tile, sub + kComputeWarps, dst, FULL);
+          if constexpr (!PREFETCH) {
+            load(tile, sub, buf[0], FULL);
+            if (r + 1 == PER_WARP) {
+              mbar_wait(&mb_tile[(k + 1) & kRingMask], (uint32_t)(((k + 1) / kTileRing) & 1));
+              next = s_tile[(k + 1) & kRingMask];
+            }
           } else {
-            mbar_wait(&mb_tile[(k + 1) & kRingMask], (uint32_t)(((k + 1) / kTileRing) & 1));
-            next = s_tile[(k + 1) & kRingMask];
-            if (next < ntiles) load(next, warp, dst, false);
+            const int cur = PING ? (r & 1) : 0;
+            if (!PING) {
+#pragma unroll
+              for (int j = 0; j < IT; ++j)
+#pragma unroll
+                for (int c = 0; c < IN; ++c)
+#pragma unroll
+                  for (int v = 0; v < V; ++v) held[j][c][v] = buf[0][j][c][v];
+            }
+            T (&dst)[IT][IN][V] = PING ? buf[cur ^ 1] : buf[0];
+            if (r + 1 < PER_WARP) {
+              load(tile, sub + kComputeWarps, dst, FULL);
+            } else {
+              mbar_wait(&mb_tile[(k + 1) & kRingMask], (uint32_t)(((k + 1) / kTileRing) & 1));
+              next = s_tile[(k + 1) & kRingMask];
+              if (next < ntiles) load(next, warp, dst, false);
+            }
           }
-          const T (&plane)[IT][IN][V] = PING ? buf[cur] : held;
+          const T (&plane)[IT][IN][V] = (PREFETCH && !PING) ? held : buf[PREFETCH ? (r & 1) : 0];
           const int rem = FULL ? SUB : remaining(tile, sub);
           uint8_t* fl = FLAGS ? flags + tile * BT + (int64_t)sub * SUB : nullptr;
           T res[IT][OUT][V];

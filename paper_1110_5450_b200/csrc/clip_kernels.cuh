@@ -62,8 +62,8 @@ template <typename T, class Op> __host__ __device__ constexpr bool compact_headl
 }
 // The other instantiations, (compute warps, sub-tiles per tile, staged tiles), measured at
 // 1e8 segments (scripts/kernel_probe.py): fp32 3D 12 x 24 x 3 (1.18 ms vs 1.40 at 16 x 16 x 3),
-// fp64 2D 8 x 16 x 2 (2.03 ms vs 2.27 at 8 x 8 x 3); homogeneous fp32 8 x 16 x 3 (1.83 ms,
-// better than 12 x 24 or 16 x 16, which spill).
+// fp64 2D 8 x 16 x 2 (2.03 ms vs 2.27 at 8 x 8 x 3); homogeneous fp32 12 x 24 x 3 without
+// the register prefetch (see compact_prefetch).
 #ifndef CLIPSEG_F32_3D_W
 #define CLIPSEG_F32_3D_W 12
 #endif
@@ -92,10 +92,10 @@ template <typename T, class Op> __host__ __device__ constexpr bool compact_headl
 #define CLIPSEG_F64_3D_B 2
 #endif
 #ifndef CLIPSEG_F32_H_W
-#define CLIPSEG_F32_H_W 8
+#define CLIPSEG_F32_H_W 12
 #endif
 #ifndef CLIPSEG_F32_H_N
-#define CLIPSEG_F32_H_N 16
+#define CLIPSEG_F32_H_N 24
 #endif
 #ifndef CLIPSEG_F32_H_B
 #define CLIPSEG_F32_H_B 3
@@ -128,6 +128,15 @@ template <typename T, class Op> __host__ __device__ constexpr int compact_subtil
 }
 template <typename T, class Op> __host__ __device__ constexpr int compact_buffers() {
   return compact_knobs<T, Op>().nbuf;
+}
+#ifndef CLIPSEG_HOMOG_PREFETCH
+#define CLIPSEG_HOMOG_PREFETCH 0
+#endif
+// Next-sub-tile loads in flight in a second register buffer — except for fp32 homogeneous
+// rows (8 planes), whose registers buy more warps instead: 12 x 24 without the prefetch
+// 1.77 ms vs 8 x 16 with it 1.79 ms at 1e8.
+template <typename T, class Op> __host__ __device__ constexpr bool compact_prefetch() {
+  return !(Op::IN == 8 && sizeof(T) == 4) || CLIPSEG_HOMOG_PREFETCH;
 }
 template <typename T, class Op> __host__ __device__ constexpr int compact_min_blocks() {
   return compact_headline<T, Op>() ? CLIPSEG_MINB_F32_2D : 1;
