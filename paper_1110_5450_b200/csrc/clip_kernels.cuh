@@ -135,8 +135,13 @@ template <typename T, class Op> __host__ __device__ constexpr int compact_buffer
 // Next-sub-tile loads in flight in a second register buffer — except for fp32 homogeneous
 // rows (8 planes), whose registers buy more warps instead: 12 x 24 without the prefetch
 // 1.77 ms vs 8 x 16 with it 1.79 ms at 1e8.
+#ifndef CLIPSEG_F32_3D_PREFETCH
+#define CLIPSEG_F32_3D_PREFETCH 1
+#endif
 template <typename T, class Op> __host__ __device__ constexpr bool compact_prefetch() {
-  return !(Op::IN == 8 && sizeof(T) == 4) || CLIPSEG_HOMOG_PREFETCH;
+  return Op::IN == 8 && sizeof(T) == 4   ? CLIPSEG_HOMOG_PREFETCH != 0
+         : Op::IN == 6 && sizeof(T) == 4 ? CLIPSEG_F32_3D_PREFETCH != 0
+                                         : true;
 }
 template <typename T, class Op> __host__ __device__ constexpr int compact_min_blocks() {
   return compact_headline<T, Op>() ? CLIPSEG_MINB_F32_2D : 1;
