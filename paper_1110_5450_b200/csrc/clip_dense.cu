@@ -10,31 +10,59 @@
 
 namespace clipseg {
 
-// (occupancy over registers: the homogeneous fp32 instantiation spills a little at 3
-// blocks/SM and is still faster than at 1 or 2 — measured 3.05 / 4.9 / 4.2 ms at 1e8)
+#ifndef CLIPSEG_DENSE_HOMOG_PREFETCH
+#define CLIPSEG_DENSE_HOMOG_PREFETCH 0  // fp32 homogeneous: 1.42 ms without vs 1.73 with (1e8)
+#endif
+#ifndef CLIPSEG_DENSE_3D_PREFETCH
+#define CLIPSEG_DENSE_3D_PREFETCH 0  // fp32 3D: 0.884 ms without vs 0.968 with (1e8)
+#endif
+#ifndef CLIPSEG_DENSE_2D_PREFETCH
+#define CLIPSEG_DENSE_2D_PREFETCH 1
+#endif
+#ifndef CLIPSEG_DENSE_F64_PREFETCH
+#define CLIPSEG_DENSE_F64_PREFETCH 1
+#endif
+#ifndef CLIPSEG_DENSE_HOMOG_MINB
+#define CLIPSEG_DENSE_HOMOG_MINB 3
+#endif
+// The next group's loads in flight while this one is clipped (registers for a second
+// group) — except where the registers buy more than the overlap (measured per case).
+template <typename T, class Op> __host__ __device__ constexpr bool dense_prefetch() {
+  return sizeof(T) == 8   ? CLIPSEG_DENSE_F64_PREFETCH != 0
+         : Op::IN == 8 ? CLIPSEG_DENSE_HOMOG_PREFETCH != 0
+         : Op::IN == 6 ? CLIPSEG_DENSE_3D_PREFETCH != 0
+                       : CLIPSEG_DENSE_2D_PREFETCH != 0;
+}
 template <typename T, class Op>
-__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 3 : 2)
+__global__ void __launch_bounds__(256, (Op::IN == 8 && sizeof(T) == 4) ? CLIPSEG_DENSE_HOMOG_MINB
+                                                                          : (sizeof(T) == 4 ? 3 : 2))
     clip_dense_kernel(const T* in, int64_t ld_in, int64_t n, typename Op::Params w, T* out, int64_t ld_out,
                       uint8_t* flags) {
   constexpr int V = Vec16<T>::N, IN = Op::IN, OUT = Op::OUT;
   const int64_t ngroups = (n + V - 1) / V;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  T nxt[IN][V];
-  if (g < ngroups) {
+  constexpr bool PREFETCH = dense_prefetch<T, Op>();
+  T nxt[PREFETCH ? IN : 1][V];
+  if (PREFETCH && g < ngroups) {
 #pragma unroll
     for (int c = 0; c < IN; ++c) load_vec<T, IN == 4>(in + c * ld_in + g * V, nxt[c]);
   }
   for (; g < ngroups; g += stride) {
     const int64_t i = g * V;
     T plane[IN][V];
+    if constexpr (PREFETCH) {
 #pragma unroll
-    for (int c = 0; c < IN; ++c)
+      for (int c = 0; c < IN; ++c)
 #pragma unroll
-      for (int v = 0; v < V; ++v) plane[c][v] = nxt[c][v];
-    if (g + stride < ngroups) {  // next group's loads in flight while this one is clipped
+        for (int v = 0; v < V; ++v) plane[c][v] = nxt[c][v];
+      if (g + stride < ngroups) {  // next group's loads in flight while this one is clipped
 #pragma unroll
-      for (int c = 0; c < IN; ++c) load_vec<T, IN == 4>(in + c * ld_in + (g + stride) * V, nxt[c]);
+        for (int c = 0; c < IN; ++c) load_vec<T, IN == 4>(in + c * ld_in + (g + stride) * V, nxt[c]);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < IN; ++c) load_vec<T, IN == 4>(in + c * ld_in + i, plane[c]);
     }
     T res[OUT][V];
     const unsigned bits = Op::template group<V, true>(plane, w, res);
