@@ -138,9 +138,13 @@ template <typename T, class Op> __host__ __device__ constexpr int compact_buffer
 #ifndef CLIPSEG_F32_3D_PREFETCH
 #define CLIPSEG_F32_3D_PREFETCH 1
 #endif
+#ifndef CLIPSEG_F32_2D_PREFETCH
+#define CLIPSEG_F32_2D_PREFETCH 1
+#endif
 template <typename T, class Op> __host__ __device__ constexpr bool compact_prefetch() {
   return Op::IN == 8 && sizeof(T) == 4   ? CLIPSEG_HOMOG_PREFETCH != 0
          : Op::IN == 6 && sizeof(T) == 4 ? CLIPSEG_F32_3D_PREFETCH != 0
+         : Op::IN == 4 && sizeof(T) == 4 ? CLIPSEG_F32_2D_PREFETCH != 0
                                          : true;
 }
 template <typename T, class Op> __host__ __device__ constexpr int compact_min_blocks() {
