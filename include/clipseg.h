@@ -168,10 +168,12 @@ int clip_tof_range_phi_f32(const float* d, const float* I, int64_t n, int64_t pi
  * labels:   int32 per pixel: the id of its final region (0 for invalid pixels);
  * nregions: (nullable) int32[nframes] final region counts; d_rounds: (nullable) device int32:
  *           rounds run including the final one without merges (max_rounds if not converged);
- * workspace: clip_cluster_workspace_bytes(...) device bytes, 256-byte aligned.
+ * workspace: clip_cluster_workspace_bytes(...) device bytes, 256-byte aligned (sized for one
+ *           part: batches run as consecutive launches of at most 64 frames).
  * Limits: nframes * height * width < 2^30.  Status: CLIP_EINVAL (bad sizes, negative or
  * non-finite params, max_rounds < 1, null pointers), CLIP_EALIGN, CLIP_ENOSPACE, CLIP_ECUDA.
- * One cooperative launch (the rounds run on the device, no host round trips). */
+ * One cooperative launch per part of the batch (the rounds run on the device, no host
+ * round trips). */
 typedef struct {
   double t_z, t_phi, alpha_z, alpha_phi;
 } clip_merge_params;

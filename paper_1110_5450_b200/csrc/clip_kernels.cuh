@@ -169,7 +169,12 @@ cudaError_t launch_shard_offsets(const int64_t* d_counts, int P, int rank, int64
 cudaError_t launch_tof_range_phi(const float* d, const float* I, int64_t n, int64_t ppf, const float* ranges,
                                  float* phi, uint8_t* code, int* kept, cudaStream_t s);
 
-// NEXT-3 (cluster.cu): round-synchronous mutual-best region merging of nframes H x W frames.
+// NEXT-3 (cluster.cu): round-synchronous mutual-best region merging of nframes H x W frames,
+// launched kClusterFrames frames at a time (the workspace holds one part).
+#ifndef CLIPSEG_CLUSTER_FRAMES
+#define CLIPSEG_CLUSTER_FRAMES 64
+#endif
+constexpr int64_t kClusterFrames = CLIPSEG_CLUSTER_FRAMES;
 size_t cluster_workspace_bytes(int64_t n);
 cudaError_t launch_cluster(const float* z, const float* phi, const uint8_t* valid, int64_t nframes, int H, int W,
                            double t_z, double t_phi, double alpha_z, double alpha_phi, int max_rounds, int* labels,

@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(256) cluster_kernel(const float* __restrict__ 
     grid.sync();
     if (merges[cur] == 0) break;  // the same value for every thread: uniform exit
   }
-  if (t0 == 0 && rounds_out) *rounds_out = round < max_rounds ? round + 1 : max_rounds;
+  if (t0 == 0 && rounds_out) atomicMax(rounds_out, round < max_rounds ? round + 1 : max_rounds);
 
   // labels: pointer jumping to the surviving region, then its id (0 for invalid pixels)
   for (;;) {
@@ -211,10 +211,11 @@ size_t cluster_workspace_bytes(int64_t n) {
   return (size_t)n * (32 + 24 + 8 + 32 + 16 + 8) + 16 * 256;
 }
 
-cudaError_t launch_cluster(const float* z, const float* phi, const uint8_t* valid, int64_t nframes, int H, int W,
-                           double t_z, double t_phi, double alpha_z, double alpha_phi, int max_rounds, int* labels,
-                           int* nregions, int* rounds_out, void* ws, cudaStream_t s) {
-  const int64_t n = nframes * (int64_t)H * W;
+// One cooperative launch for frames [f0, f0 + nf) of the batch, workspace laid out for nf.
+static cudaError_t launch_cluster_part(const float* z, const float* phi, const uint8_t* valid, int64_t nf, int H,
+                                       int W, const MergeParams& prm, int max_rounds, int* labels, int* nregions,
+                                       int* rounds_out, void* ws, cudaStream_t s) {
+  const int64_t n = nf * (int64_t)H * W;
   char* p = reinterpret_cast<char*>(ws);
   ClusterWs w;
   auto take = [&](size_t bytes) {
@@ -236,19 +237,12 @@ cudaError_t launch_cluster(const float* z, const float* phi, const uint8_t* vali
   w.cnt = reinterpret_cast<int*>(take(4 * n));
   w.parent = reinterpret_cast<int*>(take(4 * n));
   w.counts = reinterpret_cast<int*>(take(64));
-  {
-    const cudaError_t e = cudaMemsetAsync(w.counts, 0, 64, s);
-    if (e != cudaSuccess) return e;
-  }
-  MergeParams prm{t_z, t_phi, alpha_z, alpha_phi};
-  if (nregions) {
-    const cudaError_t e = cudaMemsetAsync(nregions, 0, (size_t)nframes * sizeof(int), s);
-    if (e != cudaSuccess) return e;
-  }
+  const cudaError_t e = cudaMemsetAsync(w.counts, 0, 64, s);
+  if (e != cudaSuccess) return e;
   static int blocks_per_sm = 0;
   if (!blocks_per_sm) {
-    const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, cluster_kernel, 256, 0);
-    if (e != cudaSuccess || blocks_per_sm < 1) blocks_per_sm = 1;
+    const cudaError_t e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, cluster_kernel, 256, 0);
+    if (e2 != cudaSuccess || blocks_per_sm < 1) blocks_per_sm = 1;
   }
 #ifndef CLIPSEG_CLUSTER_PIX_PER_BLOCK
 #define CLIPSEG_CLUSTER_PIX_PER_BLOCK 512  // pixels per block (128..2048 measured alike; 8192 slower)
@@ -256,9 +250,35 @@ cudaError_t launch_cluster(const float* z, const float* phi, const uint8_t* vali
   const int64_t want = (n + CLIPSEG_CLUSTER_PIX_PER_BLOCK - 1) / CLIPSEG_CLUSTER_PIX_PER_BLOCK;
   const int64_t cap = (int64_t)device_sm_count() * blocks_per_sm;
   const int grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
-  void* args[] = {(void*)&z, (void*)&phi, (void*)&valid, (void*)&nframes, (void*)&H, (void*)&W, (void*)&prm,
+  MergeParams prm_copy = prm;
+  void* args[] = {(void*)&z, (void*)&phi, (void*)&valid, (void*)&nf, (void*)&H, (void*)&W, (void*)&prm_copy,
                   (void*)&w, (void*)&max_rounds, (void*)&labels, (void*)&nregions, (void*)&rounds_out};
   return cudaLaunchCooperativeKernel((const void*)cluster_kernel, dim3(grid), dim3(256), args, 0, s);
+}
+
+cudaError_t launch_cluster(const float* z, const float* phi, const uint8_t* valid, int64_t nframes, int H, int W,
+                           double t_z, double t_phi, double alpha_z, double alpha_phi, int max_rounds, int* labels,
+                           int* nregions, int* rounds_out, void* ws, cudaStream_t s) {
+  const MergeParams prm{t_z, t_phi, alpha_z, alpha_phi};
+  if (nregions) {
+    const cudaError_t e = cudaMemsetAsync(nregions, 0, (size_t)nframes * sizeof(int), s);
+    if (e != cudaSuccess) return e;
+  }
+  if (rounds_out) {
+    const cudaError_t e = cudaMemsetAsync(rounds_out, 0, sizeof(int), s);
+    if (e != cudaSuccess) return e;
+  }
+  // Frames are independent: big batches run as consecutive launches of at most
+  // kClusterFrames frames, whose live graphs stay closer to L2 (measured 0.88 ms per frame
+  // for 256 frames this way vs 1.10 in one launch); the workspace is sized for one part.
+  const int64_t P = (int64_t)H * W;
+  for (int64_t f0 = 0; f0 < nframes; f0 += kClusterFrames) {
+    const int64_t nf = nframes - f0 < kClusterFrames ? nframes - f0 : kClusterFrames;
+    const cudaError_t e = launch_cluster_part(z + f0 * P, phi + f0 * P, valid + f0 * P, nf, H, W, prm, max_rounds,
+                                              labels + f0 * P, nregions ? nregions + f0 : nullptr, rounds_out, ws, s);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 }  // namespace clipseg

@@ -87,3 +87,10 @@ def test_full_size_frames(torch, cs):
     z, ph, v, gt = scenes.batch(2, 204, 204, seed=11)
     lab = check(torch, cs, z, ph, v)
     assert 2 <= len(np.unique(lab[0])) <= 50
+
+
+def test_batch_split_into_launches(torch, cs):
+    """More frames than one launch takes (64): consecutive launches, per-frame labels and
+    counts still identical to the oracle, rounds = the maximum over all frames."""
+    z, ph, v, gt = scenes.batch(67, 12, 14, seed=21)
+    check(torch, cs, z, ph, v)
