@@ -342,7 +342,7 @@ int clip_tof_range_phi_f32(const float* d, const float* I, int64_t n, int64_t pi
 
 size_t clip_cluster_workspace_bytes(int64_t nframes, int height, int width) {
   if (nframes < 0 || height < 1 || width < 1) return 0;
-  const int64_t part = nframes < kClusterFrames ? nframes : kClusterFrames;  // frames per launch
+  const int64_t part = cluster_part_frames(nframes);  // frames per launch
   return cluster_workspace_bytes(part * (int64_t)height * width) + 4096;
 }
 

@@ -169,12 +169,20 @@ cudaError_t launch_shard_offsets(const int64_t* d_counts, int P, int rank, int64
 cudaError_t launch_tof_range_phi(const float* d, const float* I, int64_t n, int64_t ppf, const float* ranges,
                                  float* phi, uint8_t* code, int* kept, cudaStream_t s);
 
-// NEXT-3 (cluster.cu): round-synchronous mutual-best region merging of nframes H x W frames,
-// launched kClusterFrames frames at a time (the workspace holds one part).
-#ifndef CLIPSEG_CLUSTER_FRAMES
-#define CLIPSEG_CLUSTER_FRAMES 64
-#endif
-constexpr int64_t kClusterFrames = CLIPSEG_CLUSTER_FRAMES;
+// NEXT-3 (cluster.cu): round-synchronous mutual-best region merging of nframes H x W frames.
+// Two schedules (measured, scripts/cluster_probe.py, 204^2 frames): small batches run every
+// round grid-wide (all SMs on each frame's rounds: 11.6 ms for 1 frame, 1.70 ms per frame at
+// 16, 0.98 at 47), batches of >= kClusterPerFrameMin frames give each frame its own
+// 1024-thread block with block barriers (1.03 ms per frame at 48, 0.79 at 64, 0.34 at 296).
+// Each schedule processes at most cluster_part_frames() frames per launch; the workspace
+// holds one part.
+constexpr int64_t kClusterPerFrameMin = 64;
+constexpr int64_t kClusterGridFrames = 64;
+constexpr int64_t kClusterBlockFrames = 592;
+__host__ __device__ constexpr int64_t cluster_part_frames(int64_t nframes) {
+  return nframes >= kClusterPerFrameMin ? (nframes < kClusterBlockFrames ? nframes : kClusterBlockFrames)
+                                        : (nframes < kClusterGridFrames ? nframes : kClusterGridFrames);
+}
 size_t cluster_workspace_bytes(int64_t n);
 cudaError_t launch_cluster(const float* z, const float* phi, const uint8_t* valid, int64_t nframes, int H, int W,
                            double t_z, double t_phi, double alpha_z, double alpha_phi, int max_rounds, int* labels,

@@ -203,6 +203,164 @@ __global__ void __launch_bounds__(256) cluster_kernel(const float* __restrict__ 
   }
 }
 
+// One block per frame: frames are independent, so a frame's rounds need only block-level
+// barriers (__syncthreads) instead of grid-wide ones, and many frames run concurrently.  The
+// phases and every decision are those of cluster_kernel, restricted to the frame's pixels;
+// the frame's live lists live in its slice of the workspace, their counters in shared memory.
+#ifndef CLIPSEG_CLUSTER_FRAME_THREADS
+#define CLIPSEG_CLUSTER_FRAME_THREADS 1024
+#endif
+__global__ void __launch_bounds__(CLIPSEG_CLUSTER_FRAME_THREADS) cluster_frame_kernel(const float* __restrict__ z,
+                                                              const float* __restrict__ phi,
+                                                              const uint8_t* __restrict__ valid, int64_t nframes,
+                                                              int H, int W, MergeParams prm, ClusterWs w,
+                                                              int max_rounds, int* __restrict__ labels,
+                                                              int* __restrict__ nregions, int* __restrict__ rounds_out) {
+  __shared__ int ecount[2], rcount[2], merges[2], changed, roots;
+  const int64_t P = (int64_t)H * W;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int64_t f = blockIdx.x; f < nframes; f += gridDim.x) {
+    const int64_t base = f * P;
+    int* const ea0 = w.ea[0] + 2 * base;
+    int* const ea1 = w.ea[1] + 2 * base;
+    int* const eb0 = w.eb[0] + 2 * base;
+    int* const eb1 = w.eb[1] + 2 * base;
+    int* const rl0 = w.rl[0] + base;
+    int* const rl1 = w.rl[1] + base;
+    unsigned long long* const ed = w.ed + 2 * base;
+    if (tid == 0) {
+      ecount[0] = ecount[1] = rcount[0] = rcount[1] = merges[0] = merges[1] = roots = 0;
+    }
+    __syncthreads();
+    for (int64_t q = tid; q < P; q += nt) {
+      const int64_t g = base + q;
+      const bool v = valid[g] != 0;
+      w.cnt[g] = v;
+      w.parent[g] = (int)g;
+      w.bestid[0][g] = 0;
+      w.bestd[0][g] = ~0ull;
+      const double zz = v ? (double)z[g] : 0.0, pp = v ? (double)phi[g] : 0.0;
+      w.sz[g] = zz;
+      w.sp[g] = pp;
+      w.m[g] = make_double2(zz, pp);
+      const int x = (int)(q % W), y = (int)(q / W);
+      const bool r = v && x + 1 < W && valid[g + 1] != 0, d = v && y + 1 < H && valid[g + W] != 0;
+      int slot = append_slot(ecount + 0, r);
+      if (r) {
+        ea0[slot] = (int)g;
+        eb0[slot] = (int)(g + 1);
+      }
+      slot = append_slot(ecount + 0, d);
+      if (d) {
+        ea0[slot] = (int)g;
+        eb0[slot] = (int)(g + W);
+      }
+      slot = append_slot(rcount + 0, v);
+      if (v) rl0[slot] = (int)g;
+    }
+    __syncthreads();
+    int round = 0;
+    for (; round < max_rounds; ++round) {
+      const int cur = round & 1, nxt = cur ^ 1;
+      int* const eac = cur ? ea1 : ea0;  // this round's lists (pointers, not indexed arrays:
+      int* const ebc = cur ? eb1 : eb0;  // no local memory)
+      int* const ean = cur ? ea0 : ea1;
+      int* const ebn = cur ? eb0 : eb1;
+      int* const rlc = cur ? rl1 : rl0;
+      int* const rln = cur ? rl0 : rl1;
+      const int ne = ecount[cur];
+      if (tid == 0) rcount[nxt] = 0;
+      for (int e = tid; e < ne; e += nt) {  // A
+        const int a = w.parent[eac[e]], b = w.parent[ebc[e]];
+        const bool live = a != b;
+        const int slot = append_slot(ecount + nxt, live);
+        if (!live) continue;
+        ean[slot] = a;
+        ebn[slot] = b;
+        double dist;
+        const bool ok = eq1(w, a, b, prm, &dist);
+        const unsigned long long bits = ok ? (unsigned long long)__double_as_longlong(dist) : ~0ull;
+        ed[slot] = bits;
+        if (ok) {
+          atomicMin(w.bestd[cur] + a, bits);
+          atomicMin(w.bestd[cur] + b, bits);
+        }
+      }
+      __syncthreads();
+      const int ne2 = ecount[nxt];
+      if (tid == 0) ecount[cur] = 0;
+      for (int e = tid; e < ne2; e += nt) {  // B
+        const unsigned long long bits = ed[e];
+        if (bits == ~0ull) continue;
+        const int a = ean[e], b = ebn[e];
+        if (bits == w.bestd[cur][a]) atomicMax(w.bestid[cur] + a, (int)(b - base) + 1);
+        if (bits == w.bestd[cur][b]) atomicMax(w.bestid[cur] + b, (int)(a - base) + 1);
+      }
+      __syncthreads();
+      const int nr = rcount[cur];
+      if (tid == 0) merges[nxt] = 0;
+      for (int i = tid; i < nr; i += nt) {  // C
+        const int g = rlc[i];
+        const int bi = w.bestid[cur][g];
+        const int me = (int)(g - base) + 1;
+        const int pg = (int)(base + bi - 1);
+        const bool mutual = bi != 0 && w.bestid[cur][pg] == me;
+        const bool absorbed = mutual && me < bi;
+        if (absorbed) {
+          w.parent[g] = pg;
+        } else if (mutual) {
+          const int c = w.cnt[g] + w.cnt[pg];
+          const double s1 = __dadd_rn(w.sz[g], w.sz[pg]), s2 = __dadd_rn(w.sp[g], w.sp[pg]);
+          w.cnt[g] = c;
+          w.sz[g] = s1;
+          w.sp[g] = s2;
+          w.m[g] = make_double2(__ddiv_rn(s1, (double)c), __ddiv_rn(s2, (double)c));
+          atomicAdd(merges + cur, 1);
+        }
+        const int slot = append_slot(rcount + nxt, !absorbed);
+        if (!absorbed) {
+          rln[slot] = g;
+          w.bestid[nxt][g] = 0;
+          w.bestd[nxt][g] = ~0ull;
+        }
+      }
+      __syncthreads();
+      if (merges[cur] == 0) break;  // block-uniform
+    }
+    if (tid == 0 && rounds_out) atomicMax(rounds_out, round < max_rounds ? round + 1 : max_rounds);
+    for (;;) {  // pointer jumping within the frame
+      if (tid == 0) changed = 0;
+      __syncthreads();
+      int ch = 0;
+      for (int64_t q = tid; q < P; q += nt) {
+        const int64_t g = base + q;
+        const int pp = w.parent[g], p2 = w.parent[pp];
+        if (p2 != pp) {
+          w.parent[g] = p2;
+          ch = 1;
+        }
+      }
+      if (ch) atomicOr(&changed, 1);
+      __syncthreads();
+      const int done = changed == 0;
+      __syncthreads();
+      if (done) break;
+    }
+    int mine = 0;
+    for (int64_t q = tid; q < P; q += nt) {
+      const int64_t g = base + q;
+      const bool v = valid[g] != 0;
+      const int root = w.parent[g];
+      labels[g] = v ? (int)(root - base) + 1 : 0;
+      mine += v && root == (int)g;
+    }
+    if (mine) atomicAdd(&roots, mine);
+    __syncthreads();
+    if (tid == 0 && nregions) nregions[f] = roots;
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 size_t cluster_workspace_bytes(int64_t n) {
@@ -214,7 +372,7 @@ size_t cluster_workspace_bytes(int64_t n) {
 // One cooperative launch for frames [f0, f0 + nf) of the batch, workspace laid out for nf.
 static cudaError_t launch_cluster_part(const float* z, const float* phi, const uint8_t* valid, int64_t nf, int H,
                                        int W, const MergeParams& prm, int max_rounds, int* labels, int* nregions,
-                                       int* rounds_out, void* ws, cudaStream_t s) {
+                                       int* rounds_out, void* ws, bool per_frame, cudaStream_t s) {
   const int64_t n = nf * (int64_t)H * W;
   char* p = reinterpret_cast<char*>(ws);
   ClusterWs w;
@@ -251,6 +409,12 @@ static cudaError_t launch_cluster_part(const float* z, const float* phi, const u
   const int64_t cap = (int64_t)device_sm_count() * blocks_per_sm;
   const int grid = (int)(want < cap ? (want > 0 ? want : 1) : cap);
   MergeParams prm_copy = prm;
+  if (per_frame) {  // one block per frame (a grid-stride loop over the part's frames)
+    const int fgrid = (int)(nf < (1 << 20) ? nf : (1 << 20));
+    cluster_frame_kernel<<<fgrid, CLIPSEG_CLUSTER_FRAME_THREADS, 0, s>>>(z, phi, valid, nf, H, W, prm_copy, w,
+                                                                         max_rounds, labels, nregions, rounds_out);
+    return cudaGetLastError();
+  }
   void* args[] = {(void*)&z, (void*)&phi, (void*)&valid, (void*)&nf, (void*)&H, (void*)&W, (void*)&prm_copy,
                   (void*)&w, (void*)&max_rounds, (void*)&labels, (void*)&nregions, (void*)&rounds_out};
   return cudaLaunchCooperativeKernel((const void*)cluster_kernel, dim3(grid), dim3(256), args, 0, s);
@@ -268,14 +432,17 @@ cudaError_t launch_cluster(const float* z, const float* phi, const uint8_t* vali
     const cudaError_t e = cudaMemsetAsync(rounds_out, 0, sizeof(int), s);
     if (e != cudaSuccess) return e;
   }
-  // Frames are independent: big batches run as consecutive launches of at most
-  // kClusterFrames frames, whose live graphs stay closer to L2 (measured 0.88 ms per frame
-  // for 256 frames this way vs 1.10 in one launch); the workspace is sized for one part.
+  // Frames are independent: batches run as consecutive launches of at most
+  // cluster_part_frames() frames with the schedule chosen by the batch size (clip_kernels.cuh);
+  // the workspace is sized for one part.
   const int64_t P = (int64_t)H * W;
-  for (int64_t f0 = 0; f0 < nframes; f0 += kClusterFrames) {
-    const int64_t nf = nframes - f0 < kClusterFrames ? nframes - f0 : kClusterFrames;
+  const bool per_frame = nframes >= kClusterPerFrameMin;
+  const int64_t part = cluster_part_frames(nframes);
+  for (int64_t f0 = 0; f0 < nframes; f0 += part) {
+    const int64_t nf = nframes - f0 < part ? nframes - f0 : part;
     const cudaError_t e = launch_cluster_part(z + f0 * P, phi + f0 * P, valid + f0 * P, nf, H, W, prm, max_rounds,
-                                              labels + f0 * P, nregions ? nregions + f0 : nullptr, rounds_out, ws, s);
+                                              labels + f0 * P, nregions ? nregions + f0 : nullptr, rounds_out, ws,
+                                              per_frame, s);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

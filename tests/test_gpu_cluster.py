@@ -89,8 +89,10 @@ def test_full_size_frames(torch, cs):
     assert 2 <= len(np.unique(lab[0])) <= 50
 
 
-def test_batch_split_into_launches(torch, cs):
-    """More frames than one launch takes (64): consecutive launches, per-frame labels and
-    counts still identical to the oracle, rounds = the maximum over all frames."""
-    z, ph, v, gt = scenes.batch(67, 12, 14, seed=21)
+@pytest.mark.parametrize("nframes,h,w", [(63, 12, 14), (67, 12, 14), (593, 8, 9)])
+def test_batch_schedules(torch, cs, nframes, h, w):
+    """Both schedules (grid-wide rounds below 64 frames, one block per frame from 64) and
+    batches split into several launches (more than 592 frames): per-frame labels and counts
+    identical to the oracle, rounds = the maximum over all frames."""
+    z, ph, v, gt = scenes.batch(nframes, h, w, seed=21 + nframes)
     check(torch, cs, z, ph, v)
