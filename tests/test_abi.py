@@ -135,6 +135,33 @@ def test_tof_validation(cs):
     assert f(FAKE, FAKE, 10, 10, FAKE, FAKE, None, FAKE + 2, None) == cs.CLIP_EALIGN
 
 
+def test_cluster_validation(cs):
+    prm = cs.clip_merge_params(0.04, 0.009, 8 / 3.141592653589793, 4 / 3)
+    ws = 1 << 32
+    need = cs.clip_cluster_workspace_bytes(2, 8, 8)
+    assert need > 0 and cs.clip_cluster_workspace_bytes(-1, 8, 8) == 0 and cs.clip_cluster_workspace_bytes(1, 0, 8) == 0
+    # batches run in parts: the workspace of a huge batch is that of one part
+    assert cs.clip_cluster_workspace_bytes(10**5, 204, 204) == cs.clip_cluster_workspace_bytes(592, 204, 204)
+    f = cs.clip_cluster_frames
+
+    def call(F=2, H=8, W=8, p=prm, rounds=100, z=FAKE, ph=FAKE, v=FAKE, lab=FAKE, nreg=None, d_r=None, w=ws,
+             wb=None):
+        return f(z, ph, v, F, H, W, ctypes.byref(p) if p is not None else None, rounds, lab, nreg, d_r, w,
+                 need if wb is None else wb, None)
+    assert call(F=-1) == cs.CLIP_EINVAL
+    assert call(H=0) == cs.CLIP_EINVAL
+    assert call(p=None) == cs.CLIP_EINVAL
+    assert call(rounds=0) == cs.CLIP_EINVAL
+    assert call(p=cs.clip_merge_params(-1.0, 0.009, 1.0, 1.0)) == cs.CLIP_EINVAL
+    assert call(p=cs.clip_merge_params(float("nan"), 0.009, 1.0, 1.0)) == cs.CLIP_EINVAL
+    assert call(F=0) == cs.CLIP_OK                                   # nothing to do, no launch
+    assert call(z=None) == cs.CLIP_EINVAL
+    assert call(w=ws + 16) == cs.CLIP_EALIGN                         # workspace 256-byte aligned
+    assert call(lab=FAKE + 2) == cs.CLIP_EALIGN
+    assert call(wb=need - 1) == cs.CLIP_ENOSPACE
+    assert call(F=1 << 20, H=1 << 10, W=1 << 10) == cs.CLIP_EINVAL  # more than 2^30 pixels
+
+
 def test_shard_offsets_validation(cs):
     assert cs.clip_shard_offsets(FAKE, 0, 0, FAKE, FAKE, None) == cs.CLIP_EINVAL
     assert cs.clip_shard_offsets(FAKE, 2, 2, FAKE, FAKE, None) == cs.CLIP_EINVAL
