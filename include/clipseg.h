@@ -169,11 +169,13 @@ int clip_tof_range_phi_f32(const float* d, const float* I, int64_t n, int64_t pi
  * nregions: (nullable) int32[nframes] final region counts; d_rounds: (nullable) device int32:
  *           rounds run including the final one without merges (max_rounds if not converged);
  * workspace: clip_cluster_workspace_bytes(...) device bytes, 256-byte aligned (sized for one
- *           part: batches run as consecutive launches of at most 64 frames).
+ *           part: batches of more than 592 frames run as consecutive launches of at most
+ *           592 frames each, reusing the workspace).
  * Limits: nframes * height * width < 2^30.  Status: CLIP_EINVAL (bad sizes, negative or
  * non-finite params, max_rounds < 1, null pointers), CLIP_EALIGN, CLIP_ENOSPACE, CLIP_ECUDA.
- * One cooperative launch per part of the batch (the rounds run on the device, no host
- * round trips). */
+ * One launch per part of the batch runs every round on the device (no host round trips):
+ * below 64 frames a grid-wide cooperative kernel (grid barriers between phases), from 64
+ * frames one 1024-thread block per frame (block barriers). */
 typedef struct {
   double t_z, t_phi, alpha_z, alpha_phi;
 } clip_merge_params;
