@@ -410,7 +410,7 @@ __global__ void __launch_bounds__(CompactShape<T, Op, INDEX>::kThreads, CompactS
 #pragma unroll
           for (int j = 0; j < IT; ++j) {
             const int o = (32 * j + lane) * V;
-            vis[j] = Op::template group<V, false>(plane[j], w, res[j]);
+            vis[j] = group_chunked<Op, false>(plane[j], w, res[j]);
             if (!FULL) vis[j] &= (o >= rem) ? 0u : (o + V <= rem ? (1u << V) - 1u : (1u << (rem - o)) - 1u);
             if (FLAGS) {
 #if CLIPSEG_MUL_FLAGS

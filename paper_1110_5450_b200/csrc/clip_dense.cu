@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(256, (Op::IN == 8 && sizeof(T) == 4) ? CLIPSEG
       for (int c = 0; c < IN; ++c) load_vec<T, IN == 4>(in + c * ld_in + i, plane[c]);
     }
     T res[OUT][V];
-    const unsigned bits = Op::template group<V, true>(plane, w, res);
+    const unsigned bits = group_chunked<Op, true>(plane, w, res);
     uint32_t vis = 0;  // one flag byte per segment
 #pragma unroll
     for (int v = 0; v < V; ++v) vis |= ((bits >> v) & 1u) << (8 * v);

@@ -13,6 +13,7 @@ namespace clipseg {
 // NAN_FILL writes R8's qNaN into invisible rows).
 template <typename T, int D> struct BoxOp {  // axis-aligned closed box, D = 2, 3 (rules R1..R10)
   static constexpr int IN = 2 * D, OUT = 2 * D;
+  static constexpr int GV = 4;  // whole groups (V <= 4)
   typedef Window<T, D> Params;
   template <int V, bool NAN_FILL>
   static __device__ __forceinline__ unsigned group(const T (&pl)[IN][V], const Params& w, T (&res)[OUT][V]) {
@@ -22,14 +23,55 @@ template <typename T, int D> struct BoxOp {  // axis-aligned closed box, D = 2, 
 struct NoParams {
   int unused;
 };
+#ifndef CLIPSEG_HOMOG_GV_F32
+#define CLIPSEG_HOMOG_GV_F32 2      // segments per group_chunked call, fp32 homogeneous output
+#endif
+#ifndef CLIPSEG_HOMOG_GV_F32_NDC
+#define CLIPSEG_HOMOG_GV_F32_NDC 1  // ... fp32 NDC output
+#endif
+#ifndef CLIPSEG_HOMOG_GV_F64
+#define CLIPSEG_HOMOG_GV_F64 2
+#endif
 template <typename T, bool NDC> struct HomogOp {  // NEXT-1: homogeneous clip space (rules H1..H10)
   static constexpr int IN = 8, OUT = NDC ? 6 : 8;
+  // Segments clipped per call: the six-plane rules of 4 segments at once need more than 128
+  // registers (spills at 80: 168 B); chunks of 2 (1 with the NDC divides) do not, measured
+  // at 1e8 fp32 (profiles/ab_log.md): dense 1.43 -> 1.21 ms and compacting 1.78 -> 1.56 ms
+  // homogeneous output, 1.66 -> 1.30 and 2.40 -> 2.02 ms NDC output; fp64 unchanged.
+  static constexpr int GV = sizeof(T) == 8 ? CLIPSEG_HOMOG_GV_F64 : (NDC ? CLIPSEG_HOMOG_GV_F32_NDC : CLIPSEG_HOMOG_GV_F32);
   typedef NoParams Params;
   template <int V, bool NAN_FILL>
   static __device__ __forceinline__ unsigned group(const T (&pl)[IN][V], const Params&, T (&res)[OUT][V]) {
     return homog_group<T, V, NAN_FILL, NDC>(pl, res);
   }
 };
+
+// Op::group over V segments in chunks of Op::GV (a power of two): bounds the live state of ops
+// whose per-segment work needs many registers (the homogeneous clipper's 6 planes).
+template <class Op, bool NAN_FILL, typename T, int V>
+__device__ __forceinline__ unsigned group_chunked(const T (&pl)[Op::IN][V], const typename Op::Params& w,
+                                                  T (&res)[Op::OUT][V]) {
+  constexpr int GV = Op::GV;
+  if constexpr (GV >= V) {
+    return Op::template group<V, NAN_FILL>(pl, w, res);
+  } else {
+    unsigned bits = 0;
+#pragma unroll
+    for (int h = 0; h < V / GV; ++h) {
+      T pg[Op::IN][GV], rg[Op::OUT][GV];
+#pragma unroll
+      for (int c = 0; c < Op::IN; ++c)
+#pragma unroll
+        for (int j = 0; j < GV; ++j) pg[c][j] = pl[c][h * GV + j];
+      bits |= Op::template group<GV, NAN_FILL>(pg, w, rg) << (h * GV);
+#pragma unroll
+      for (int c = 0; c < Op::OUT; ++c)
+#pragma unroll
+        for (int j = 0; j < GV; ++j) res[c][h * GV + j] = rg[c][j];
+    }
+    return bits;
+  }
+}
 
 // Workspace of the compacting kernel: a 128-byte header (tile-claim counter) followed by
 // one 64-bit look-back status word per tile.
