@@ -63,9 +63,18 @@ namespace {
 constexpr unsigned long long kFlagA = 1ull << 62;
 constexpr unsigned long long kFlagP = 2ull << 62;
 constexpr unsigned long long kValueMask = (1ull << 62) - 1;
-constexpr int kScanPerLane = 16;                     // scanner: 512 tiles per probe
+#ifndef CLIPSEG_SCAN_PER_LANE
+#define CLIPSEG_SCAN_PER_LANE 2  // scanner: lanes probe 2 tiles each (16: +1.6 % at 1e9, profiles/r01_summary.md)
+#endif
+#ifndef CLIPSEG_SCANNER_MAX_BACKOFF
+#define CLIPSEG_SCANNER_MAX_BACKOFF 0  // scanner: longest sleep between empty probes (0: spin; block 0 computes nothing)
+#endif
+constexpr int kScanPerLane = CLIPSEG_SCAN_PER_LANE;  // scanner: 32 x this tiles per probe
 #ifndef CLIPSEG_POLL_NS
 #define CLIPSEG_POLL_NS 500        // scan warp: sleep between polls of its tile's prefix
+#endif
+#ifndef CLIPSEG_PRE_SLEEP_NS
+#define CLIPSEG_PRE_SLEEP_NS 0     // compute warps: sleep between tests of a tile's offsets (0: suspending try_wait)
 #endif
 #ifndef CLIPSEG_SCAN_SLEEP_NS
 #define CLIPSEG_SCAN_SLEEP_NS 256  // scan warp: sleep between tests of its mbarriers
@@ -155,8 +164,8 @@ __device__ __noinline__ void global_scanner(unsigned long long* status, int64_t 
     const int fl = xmask ? __ffs(xmask) - 1 : 32;
     const int ready = (fl == 32) ? 32 * M : fl * M + __shfl_sync(0xFFFFFFFFu, myx, fl & 31);
     if (ready == 0) {
-      __nanosleep(backoff);
-      backoff = backoff < 256 ? 2 * backoff : 256;
+      if (CLIPSEG_SCANNER_MAX_BACKOFF > 0) __nanosleep(backoff);
+      backoff = backoff < CLIPSEG_SCANNER_MAX_BACKOFF ? 2 * backoff : CLIPSEG_SCANNER_MAX_BACKOFF;
       continue;
     }
     backoff = 32;
@@ -500,7 +509,8 @@ __global__ void __launch_bounds__(CompactShape<T, Op, INDEX>::kThreads, CompactS
     constexpr int Q = NBUF - 2;
     if (pend[Q] < ntiles) {
       const int pb = pbuf[Q];
-      mbar_wait(&mb_pre[pb], ppar[Q]);  // its offsets are published
+      if (CLIPSEG_PRE_SLEEP_NS > 0) mbar_wait_sleepy(&mb_pre[pb], ppar[Q], CLIPSEG_PRE_SLEEP_NS);
+      else mbar_wait(&mb_pre[pb], ppar[Q]);  // its offsets are published
       if (warp == 0 && lane == 0) CLIP_TRACE(pend[Q], 6, trace_now());
       const int64_t prefix = s_prefix[pb];
       const T* stg = stage + (size_t)pb * NSUB * SLOT;
