@@ -96,21 +96,22 @@ template <typename T> __host__ __device__ constexpr int compact_items() { return
 #define CLIPSEG_MINB_F32_2D 1      // resident blocks per SM the register budget targets
 #endif
 // fp32 2D (the bench workload): one block per SM, 16 compute warps, 4096-segment tiles,
-// 3 staged (~203 KB); fp32 3D: 16 warps, 2048-segment tiles; fp64: 8 compute warps and
+// 3 staged (~203 KB); fp32 3D: 11 warps, 2816-segment tiles; fp64: 8 compute warps and
 // 1024-segment tiles, so the wider rows keep enough registers; homogeneous (8 input
 // planes): fp32 8 warps x 2048-segment tiles, fp64 4 warps x 1024.
 template <typename T, class Op> __host__ __device__ constexpr bool compact_headline() {
   return sizeof(T) == 4 && Op::IN == 4;
 }
 // The other instantiations, (compute warps, sub-tiles per tile, staged tiles), measured at
-// 1e8 segments (scripts/kernel_probe.py): fp32 3D 12 x 24 x 3 (1.18 ms vs 1.40 at 16 x 16 x 3),
+// 1e8 segments (scripts/kernel_probe.py): fp32 3D 11 x 22 x 3 (1.06 ms; 12 x 24 x 3 1.19 ms: 13
+// warps cap ptxas at 128 registers and spill, 12 warps allow 159; 10 x 20 1.14, 11 x 33 1.10),
 // fp64 2D 8 x 16 x 2 (2.03 ms vs 2.27 at 8 x 8 x 3); homogeneous fp32 12 x 24 x 3 without
 // the register prefetch (see compact_prefetch).
 #ifndef CLIPSEG_F32_3D_W
-#define CLIPSEG_F32_3D_W 12
+#define CLIPSEG_F32_3D_W 11
 #endif
 #ifndef CLIPSEG_F32_3D_N
-#define CLIPSEG_F32_3D_N 24
+#define CLIPSEG_F32_3D_N 22
 #endif
 #ifndef CLIPSEG_F32_3D_B
 #define CLIPSEG_F32_3D_B 3

@@ -13,8 +13,9 @@ import synth
 pytestmark = pytest.mark.gpu
 
 UNIT = {2: ([0.0, 0.0], [1.0, 1.0]), 3: ([0.0, 0.0, 0.0], [1.0, 1.0, 1.0])}
-# sizes spanning several tiles (1024 / 512 segments) and every ragged tail
-SIZES = [1, 3, 4, 5, 31, 1023, 1024, 1025, 4097, 10007, 100003, 1 << 20]
+# sizes spanning several compacting tiles (fp32 2D 4096, fp32 3D 2816, fp64 2D 2048, fp64 3D
+# 1024 segments) with exact and ragged ends
+SIZES = [1, 3, 4, 5, 31, 1023, 1024, 1025, 2815, 2816, 2817, 4097, 8448, 10007, 100003, 1 << 20]
 
 
 @pytest.fixture(scope="module")
