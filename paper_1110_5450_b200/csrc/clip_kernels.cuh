@@ -105,8 +105,9 @@ template <typename T, class Op> __host__ __device__ constexpr bool compact_headl
 // The other instantiations, (compute warps, sub-tiles per tile, staged tiles), measured at
 // 1e8 segments (scripts/kernel_probe.py): fp32 3D 11 x 22 x 3 (1.06 ms; 12 x 24 x 3 1.19 ms: 13
 // warps cap ptxas at 128 registers and spill, 12 warps allow 159; 10 x 20 1.14, 11 x 33 1.10),
-// fp64 2D 8 x 16 x 2 (2.03 ms vs 2.27 at 8 x 8 x 3); homogeneous fp32 12 x 24 x 3 without
-// the register prefetch (see compact_prefetch).
+// fp64 2D 8 x 16 x 2 (2.03 ms vs 2.27 at 8 x 8 x 3); homogeneous fp32 without the register
+// prefetch (see compact_prefetch): 15 x 15 x 3 (1.43 ms; 12 x 24 1.51, 16 x 16 1.53, 19 x 19
+// 1.75), with the NDC divides 23 x 23 x 3 (1.48 ms; 19 x 19 1.53, 15 x 15 1.69, 12 x 24 2.0).
 #ifndef CLIPSEG_F32_3D_W
 #define CLIPSEG_F32_3D_W 11
 #endif
@@ -135,10 +136,16 @@ template <typename T, class Op> __host__ __device__ constexpr bool compact_headl
 #define CLIPSEG_F64_3D_B 2
 #endif
 #ifndef CLIPSEG_F32_H_W
-#define CLIPSEG_F32_H_W 12
+#define CLIPSEG_F32_H_W 15
 #endif
 #ifndef CLIPSEG_F32_H_N
-#define CLIPSEG_F32_H_N 24
+#define CLIPSEG_F32_H_N 15
+#endif
+#ifndef CLIPSEG_F32_HN_W  // homogeneous fp32 with the NDC divides (6 output planes)
+#define CLIPSEG_F32_HN_W 23
+#endif
+#ifndef CLIPSEG_F32_HN_N
+#define CLIPSEG_F32_HN_N 23
 #endif
 #ifndef CLIPSEG_F32_H_B
 #define CLIPSEG_F32_H_B 3
@@ -157,7 +164,8 @@ struct CompactKnobs {
 };
 template <typename T, class Op> __host__ __device__ constexpr CompactKnobs compact_knobs() {
   return compact_headline<T, Op>() ? CompactKnobs{CLIPSEG_COMPUTE_WARPS, CLIPSEG_NSUB_F32_2D, CLIPSEG_NBUF_F32_2D}
-         : Op::IN == 8 ? (sizeof(T) == 4 ? CompactKnobs{CLIPSEG_F32_H_W, CLIPSEG_F32_H_N, CLIPSEG_F32_H_B}
+         : Op::IN == 8 ? (sizeof(T) == 4 ? (Op::OUT == 6 ? CompactKnobs{CLIPSEG_F32_HN_W, CLIPSEG_F32_HN_N, CLIPSEG_F32_H_B}
+                                                          : CompactKnobs{CLIPSEG_F32_H_W, CLIPSEG_F32_H_N, CLIPSEG_F32_H_B})
                                          : CompactKnobs{CLIPSEG_F64_H_W, CLIPSEG_F64_H_N, CLIPSEG_F64_H_B})
          : Op::IN == 6 ? (sizeof(T) == 4 ? CompactKnobs{CLIPSEG_F32_3D_W, CLIPSEG_F32_3D_N, CLIPSEG_F32_3D_B}
                                          : CompactKnobs{CLIPSEG_F64_3D_W, CLIPSEG_F64_3D_N, CLIPSEG_F64_3D_B})

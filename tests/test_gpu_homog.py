@@ -12,7 +12,7 @@ import synth
 
 pytestmark = pytest.mark.gpu
 
-SIZES = [1, 3, 5, 31, 1023, 1025, 2049, 10007, 300007]
+SIZES = [1, 3, 5, 31, 1023, 1025, 1920, 1921, 2049, 2944, 2945, 5888, 10007, 300007]  # incl. the fp32 compacting tile edges (1920; 2944 with NDC output)
 
 
 @pytest.fixture(scope="module")
