@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--no-next1", action="store_true", help="skip the secondary NEXT-1 (homogeneous) measurement")
     ap.add_argument("--no-next2", action="store_true", help="skip the secondary NEXT-2 (range clip + phi) measurement")
     ap.add_argument("--no-next3", action="store_true", help="skip the secondary NEXT-3 (region merging) measurement")
+    ap.add_argument("--no-next4", action="store_true", help="skip the secondary NEXT-4 (int32 exact clip) measurement")
     ap.add_argument("--no-configs", action="store_true", help="skip the BASELINE.json configs[0..3] sweep")
     return ap.parse_args()
 
@@ -286,6 +287,9 @@ def main():
     next2 = None
     if rank == 0 and world == 1 and not args.no_next2:
         next2 = run_next2(torch, clipseg, synth, dev, stream)
+    next4 = None
+    if rank == 0 and world == 1 and not args.no_next4:
+        next4 = run_next4(torch, clipseg, synth, dev, stream)
     configs = None
     if rank == 0 and world == 1 and not args.no_configs:
         configs = run_config_sweep(torch, clipseg, synth, dev, stream)
@@ -332,6 +336,7 @@ def main():
         "configs": configs,
         "next1": next1,
         "next2": next2,
+        "next4": next4,
         "next3": next3,
     }
     print(json.dumps(line), flush=True)
@@ -507,6 +512,48 @@ def run_next2(torch, clipseg, synth, dev, stream, nframes=8192, steps=20):
                          "frac": alg / (ms / 1e3) / 1e9 / peak, "kernel": "tof_range_phi_kernel",
                          "alg_bytes_per_launch": alg},
             "parity": f"{'ok' if ok else 'MISMATCH'}: 3 sampled frames, codes/counts exact, phi within 1e-6"}
+
+
+def run_next4(torch, clipseg, synth, dev, stream, n=1 << 28, steps=20):
+    """NEXT-4: int32 pixel-coordinate segments, exact rational clipping with
+    round-half-up endpoints, against the 4096^2 screen window; endpoints uniform on
+    [-2048, 6144)^2 drawn on the device by a seeded torch generator (no clipping arithmetic);
+    CUDA events on the launching stream; 2048 sampled rows checked against the oracle."""
+    import numpy as np  # noqa: PLC0415
+    from oracle import int_oracle  # noqa: PLC0415
+    S = synth.INT_SCREEN
+    lo, hi = [0, 0], [S - 1, S - 1]
+    g = torch.Generator(device=dev)
+    g.manual_seed(synth.seed_for(9))
+    planes = torch.randint(-S // 2, 3 * S // 2, (4, n), generator=g, device=dev, dtype=torch.int32)
+    out = torch.empty_like(planes)
+    flags = torch.empty(n, dtype=torch.uint8, device=dev)
+    for _ in range(3):
+        clipseg.clip_int(planes, n, lo, hi, out=out, flags=flags, stream=stream)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in ev:
+        a.record(stream)
+        clipseg.clip_int(planes, n, lo, hi, out=out, flags=flags, stream=stream)
+        b.record(stream)
+    torch.cuda.synchronize()
+    ms = statistics.median(a.elapsed_time(b) for a, b in ev)
+    alg = n * (16 + 16 + 1)
+    peak, _ = measured_peak()
+    idx = np.concatenate([np.random.default_rng(2).choice(n, 2048, replace=False), [0, n - 1]])
+    ti = torch.from_numpy(idx).to(dev)
+    hp = planes[:, ti].cpu().numpy()
+    wout, wflags = int_oracle.clip_segments_i32(hp, len(idx), lo, hi)
+    ok = bool(np.array_equal(flags[ti].cpu().numpy(), wflags)) and bool(np.array_equal(out[:, ti].cpu().numpy(), wout))
+    vis = float((flags == 1).sum().item()) / n
+    del planes, out, flags
+    return {"workload": f"NEXT-4: int32 2D segments, exact clip, {n} segments, endpoints uniform on [-{S // 2}, "
+                        f"{3 * S // 2})^2, window [0, {S - 1}]^2 (SURVEY §8(f))",
+            "value": n / (ms / 1e3), "unit": "segments/s", "ms": ms, "visible_fraction": vis,
+            "roofline": {"bound": "hbm", "achieved": alg / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": alg / (ms / 1e3) / 1e9 / peak, "kernel": "clip_int_kernel",
+                         "alg_bytes_per_launch": alg},
+            "parity": f"{'ok' if ok else 'MISMATCH'}: {len(idx)} sampled rows bit-exact vs the exact-rational oracle"}
 
 
 def run_next3(torch, clipseg, dev, stream, nframes=296, steps=3):

@@ -185,6 +185,24 @@ int clip_cluster_frames(const float* z, const float* phi, const uint8_t* valid, 
                         int32_t* nregions, int32_t* d_rounds, void* workspace, size_t workspace_bytes,
                         void* stream);
 
+/* ---- NEXT-4: integer / pixel-coordinate segments, exact clipping --------
+ * SURVEY.md §8(f) NEXT-4; PAPER.md defines no integer variant (BJ:5 only mentions one), so
+ * the rules are the float path's WEC rules (PAPER.md:29-30 macros) in exact rationals:
+ * I1 every coordinate and window bound in [-2^30, 2^30]; I2 closed window lo <= hi;
+ * I3 per edge the WECs w0, w1 of P0, P1 (x - lo, hi - x), trivial reject when both < 0,
+ *    alpha = w0 / (w0 - w1) exact, t_in = max(0, entering), t_out = min(1, leaving),
+ *    visible iff t_in <= t_out;
+ * I4 Q_e,k = P0_k + floor(d_k t_e + 1/2) (round half up, exact);
+ * I5 invisible rows hold INT32_MIN in all 4 planes; I6 flag 2 = a coordinate outside I1.
+ * in, out: 4 int32 planes x0, y0, x1, y1 (ld_in / ld_out, same layout and alignment rules
+ *          as the float calls; out == in allowed).
+ * flags:   (nullable, 4-byte aligned) n bytes: 1 visible, 0 invisible, 2 out of range.
+ * win:     host pointer; lo > hi or a bound outside [-2^30, 2^30] -> CLIP_EINVAL.
+ * Results are bit-identical to the exact-rational oracle (oracle/int_oracle.py). */
+typedef struct { int32_t lo[2], hi[2]; } clip_window_i32;
+int clip_segments_i32(const int32_t* in, int64_t ld_in, int64_t n, const clip_window_i32* win, int32_t* out,
+                      int64_t ld_out, uint8_t* flags, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -31,6 +31,10 @@ class clip_merge_params(ctypes.Structure):  # noqa: N801
                 ("alpha_phi", ctypes.c_double)]
 
 
+class clip_window_i32(ctypes.Structure):  # noqa: N801
+    _fields_ = [("lo", ctypes.c_int32 * 2), ("hi", ctypes.c_int32 * 2)]
+
+
 TABLE1 = dict(t_z=0.04, t_phi=0.009, alpha_z=8 / 3.141592653589793, alpha_phi=4 / 3)  # PAPER Table 1
 
 
@@ -60,6 +64,8 @@ def _load():
         f = getattr(L, "clip_homog_segments_compact_" + s)
         f.argtypes = [P, I64, I64, ctypes.c_int, P, I64, P, I64, U8P, P, P, SZ, P]
         f.restype = ctypes.c_int
+    L.clip_segments_i32.argtypes = [P, I64, I64, ctypes.POINTER(clip_window_i32), P, I64, U8P, P]
+    L.clip_segments_i32.restype = ctypes.c_int
     L.clip_tof_range_phi_f32.argtypes = [P, P, I64, I64, P, P, U8P, P, P]
     L.clip_tof_range_phi_f32.restype = ctypes.c_int
     L.clip_cluster_workspace_bytes.argtypes = [I64, ctypes.c_int, ctypes.c_int]
@@ -91,6 +97,7 @@ clip_host_staging_bytes = _lib.clip_host_staging_bytes
 clip_segments_compact_host_f32 = _lib.clip_segments_compact_host_f32
 clip_segments_compact_host_f64 = _lib.clip_segments_compact_host_f64
 clip_tof_range_phi_f32 = _lib.clip_tof_range_phi_f32
+clip_segments_i32 = _lib.clip_segments_i32
 clip_cluster_workspace_bytes = _lib.clip_cluster_workspace_bytes
 clip_cluster_frames = _lib.clip_cluster_frames
 clip_homog_segments_f32 = _lib.clip_homog_segments_f32
@@ -103,7 +110,7 @@ EXPORTED = ["clip_plane_stride", "clip_status_string", "clip_segments_f32", "cli
             "clip_shard_offsets", "clip_host_staging_bytes", "clip_segments_compact_host_f32",
             "clip_segments_compact_host_f64", "clip_homog_segments_f32", "clip_homog_segments_f64",
             "clip_homog_segments_compact_f32", "clip_homog_segments_compact_f64", "clip_tof_range_phi_f32",
-            "clip_cluster_workspace_bytes", "clip_cluster_frames"]
+            "clip_cluster_workspace_bytes", "clip_cluster_frames", "clip_segments_i32"]
 
 
 class ClipError(RuntimeError):
@@ -268,6 +275,23 @@ def clip_homog_compact(planes, n, ndc=False, bufs: HomogBuffers | None = None, w
              bufs.flags.data_ptr() if bufs.flags is not None else None, bufs.count.data_ptr(),
              bufs.ws.data_ptr(), bufs.ws.numel(), _stream(stream)), "clip_homog_segments_compact_" + sfx)
     return bufs
+
+
+# ---- NEXT-4: int32 segments, exact clipping ---------------------------------------------------
+def clip_int(planes, n, lo, hi, out=None, flags=None, want_flags=True, stream=None):
+    """planes: CUDA int32 (4, ld) x0, y0, x1, y1 (ld a multiple of 4, >= n); lo, hi: 2 ints.
+    Returns (out int32 (4, ld_out), flags uint8[n] or None)."""
+    torch = _torch()
+    ld = planes.shape[1]
+    if out is None:
+        out = torch.empty_like(planes)
+    if flags is None and want_flags:
+        flags = torch.empty(max(n, 4), dtype=torch.uint8, device=planes.device)
+    win = clip_window_i32((ctypes.c_int32 * 2)(*lo), (ctypes.c_int32 * 2)(*hi))
+    _check(clip_segments_i32(planes.data_ptr(), ld, n, ctypes.byref(win), out.data_ptr(), out.shape[1],
+                             flags.data_ptr() if flags is not None else None, _stream(stream)),
+           "clip_segments_i32")
+    return out, flags
 
 
 # ---- NEXT-2: range clip + phi over batched ToF frames ----------------------------------------

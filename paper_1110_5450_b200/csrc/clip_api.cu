@@ -340,6 +340,20 @@ int clip_tof_range_phi_f32(const float* d, const float* I, int64_t n, int64_t pi
                                         reinterpret_cast<cudaStream_t>(stream)));
 }
 
+int clip_segments_i32(const int32_t* in, int64_t ld_in, int64_t n, const clip_window_i32* win, int32_t* out,
+                      int64_t ld_out, uint8_t* flags, void* stream) {
+  if (n < 0 || !win) return CLIP_EINVAL;
+  const int64_t B = (int64_t)1 << 30;
+  for (int k = 0; k < 2; ++k)
+    if (win->lo[k] > win->hi[k] || win->lo[k] < -B || win->hi[k] > B) return CLIP_EINVAL;
+  if (n == 0) return CLIP_OK;
+  int st;
+  if ((st = check_planes(in, ld_in, n)) || (st = check_planes(out, ld_out, n))) return st;
+  if (flags && !aligned(flags, 4)) return CLIP_EALIGN;
+  return status_of(launch_clip_int(in, ld_in, n, win->lo, win->hi, out, ld_out, flags,
+                                   reinterpret_cast<cudaStream_t>(stream)));
+}
+
 size_t clip_cluster_workspace_bytes(int64_t nframes, int height, int width) {
   if (nframes < 0 || height < 1 || width < 1) return 0;
   const int64_t part = cluster_part_frames(nframes);  // frames per launch

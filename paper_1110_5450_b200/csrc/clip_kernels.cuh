@@ -239,6 +239,10 @@ cudaError_t launch_cluster(const float* z, const float* phi, const uint8_t* vali
                            double t_z, double t_phi, double alpha_z, double alpha_phi, int max_rounds, int* labels,
                            int* nregions, int* rounds_out, void* ws, cudaStream_t s);
 
+// NEXT-4 (clip_int.cu): int32 2D segments, exact rational clipping, round-half-up endpoints.
+cudaError_t launch_clip_int(const int32_t* in, int64_t ld_in, int64_t n, const int32_t lo[2], const int32_t hi[2],
+                            int32_t* out, int64_t ld_out, uint8_t* flags, cudaStream_t s);
+
 // Number of SMs of the current device (cached per device).
 int device_sm_count();
 

@@ -126,3 +126,30 @@ def tof_device(d_t, I_t, seed, nframes, ppf=TOF_PPF, f0=0, stream=None):
     r = np.empty((max(nframes, 1), 2), np.float32)
     assert lib().synth_tof_ranges(seed, f0, nframes, r.ctypes.data) == 0
     return r[:nframes]
+
+
+# ---- NEXT-4 inputs: int32 pixel-coordinate segments (DESIGN.md §15 recipe) ----------------
+INT_SCREEN = 4096  # window [0, 4095]^2: a 4K-class raster
+
+
+def int_segments_host(seed, n, mix="screen", ld=None):
+    """Seeded int32 planes (4, ld) x0, y0, x1, y1 (ld = plane_stride(n) by default).
+    mix "screen": endpoints uniform on [-S/2, 3S/2)^2, S = INT_SCREEN (about 1/4 of each
+    endpoint inside); "wide": uniform on [-2^30, 2^30]; "edge": small coordinates around
+    the window so endpoints hit edges, corners and ties; "range": "wide" with 1 % of the
+    coordinates pushed outside [-2^30, 2^30] (flag 2).  No clipping arithmetic here."""
+    ld = plane_stride(n) if ld is None else ld
+    rng = np.random.default_rng(seed)
+    out = np.zeros((4, ld), dtype=np.int32)
+    if mix == "screen":
+        v = rng.integers(-INT_SCREEN // 2, 3 * INT_SCREEN // 2, size=(4, n))
+    elif mix == "edge":
+        v = rng.integers(-3, INT_SCREEN // 512 + 3, size=(4, n)) * 512 + rng.integers(-2, 3, size=(4, n))
+    else:
+        B = 1 << 30
+        v = rng.integers(-B, B + 1, size=(4, n))
+        if mix == "range":
+            bad = rng.random((4, n)) < 0.01
+            v = np.where(bad, rng.choice(np.array([-(1 << 31), B + 1, -B - 1, (1 << 31) - 1]), size=(4, n)), v)
+    out[:, :n] = v.astype(np.int32)
+    return out

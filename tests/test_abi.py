@@ -187,3 +187,19 @@ def test_product_path_does_not_import_oracle():
             if fn.endswith((".py", ".cu", ".cuh", ".h")):
                 src = open(os.path.join(dp, fn)).read()
                 assert "import oracle" not in src and "clip_oracle" not in src, fn
+
+
+def test_int_validation(cs):
+    f = cs.clip_segments_i32
+    W = cs.clip_window_i32
+    ok = W((ctypes.c_int32 * 2)(0, 0), (ctypes.c_int32 * 2)(4, 4))
+    assert f(None, 32, 0, ctypes.byref(ok), None, 32, None, None) == cs.CLIP_OK  # n == 0
+    assert f(None, 32, -1, ctypes.byref(ok), None, 32, None, None) == cs.CLIP_EINVAL
+    assert f(None, 32, 1, None, None, 32, None, None) == cs.CLIP_EINVAL
+    bad = W((ctypes.c_int32 * 2)(5, 0), (ctypes.c_int32 * 2)(4, 4))
+    assert f(None, 32, 0, ctypes.byref(bad), None, 32, None, None) == cs.CLIP_EINVAL
+    big = W((ctypes.c_int32 * 2)(0, 0), (ctypes.c_int32 * 2)((1 << 30) + 1, 4))
+    assert f(None, 32, 0, ctypes.byref(big), None, 32, None, None) == cs.CLIP_EINVAL
+    assert f(None, 32, 1, ctypes.byref(ok), None, 32, None, None) == cs.CLIP_EINVAL  # null planes
+    assert f(16, 30, 1, ctypes.byref(ok), 16, 32, None, None) == cs.CLIP_EALIGN  # ld*4 % 16 != 0
+    assert f(16, 32, 1, ctypes.byref(ok), 16, 32, 2, None) == cs.CLIP_EALIGN  # flags misaligned
