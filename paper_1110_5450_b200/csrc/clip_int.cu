@@ -22,73 +22,95 @@ namespace {
 
 constexpr int32_t kFill = INT32_MIN;
 constexpr int64_t kCoordMax = (int64_t)1 << 30;
+constexpr int32_t kSmall = 1 << 14;  // 32-bit path bound
 
+template <typename I>
 struct Frac {
-  int64_t num, den;  // den > 0, 0 <= num <= den
+  I num, den;  // den > 0, 0 <= num <= den
 };
 
-// a < b for fractions with positive denominators (|num|, den <= 2^31: products < 2^62)
-__device__ __forceinline__ bool frac_lt(Frac a, Frac b) { return a.num * b.den < b.num * a.den; }
+// a < b for fractions with positive denominators (|num|, den <= 2^31: products < 2^62;
+// the 32-bit path has |num|, den <= 2^15: products < 2^30)
+template <typename I>
+__device__ __forceinline__ bool frac_lt(Frac<I> a, Frac<I> b) { return a.num * b.den < b.num * a.den; }
+
+__device__ __forceinline__ double est_quot(int64_t x, double inv) { return floor(__dmul_rn((double)x, inv)); }
+__device__ __forceinline__ float est_quot(int32_t x, float inv) { return floorf(__fmul_rn((float)x, inv)); }
+__device__ __forceinline__ double rcp(int64_t d) { return __drcp_rn((double)d); }
+__device__ __forceinline__ float rcp(int32_t d) { return __frcp_rn((float)d); }
 
 // p + round_half_up(d * t): q = floor(d num / den), r = d num - q den in [0, den); +1 when
-// 2r >= den.  No 64-bit integer division (a ~70-instruction software routine that made the
-// kernel issue-bound): q is estimated as RN(RN(d num) * inv) with inv = RN(1 / den), whose
-// relative error is below 2^-50, so |q_est - d num / den| < 2^31 * 2^-50 and floor() is off by
-// at most one; the exact int64 remainder fixes that.
-__device__ __forceinline__ int32_t lerp_round(int64_t p, int64_t d, Frac t, double inv) {
-  const int64_t x = d * t.num;
-  int64_t q = (int64_t)floor(__dmul_rn((double)x, inv));
-  int64_t r = x - q * t.den;
+// 2r >= den.  No integer division (64-bit division is a ~70-instruction software routine that
+// made the kernel issue-bound): q is estimated as RN(RN(d num) * inv) with inv = RN(1 / den).
+// 64-bit path: relative error < 3 * 2^-53 and |q| <= 2^31, so the estimate is within 2^-20 of
+// d num / den; 32-bit path: relative error < 3 * 2^-24 and |q| <= 2^15, within 2^-7.  Either
+// way floor() is off by at most one, and the exact integer remainder fixes it.
+template <typename I, typename F>
+__device__ __forceinline__ int32_t lerp_round(I p, I d, Frac<I> t, F inv) {
+  const I x = d * t.num;
+  I q = (I)est_quot(x, inv);
+  I r = x - q * t.den;
   if (r < 0) { --q; r += t.den; }
   if (r >= t.den) { ++q; r -= t.den; }
   return (int32_t)(p + q + (2 * r >= t.den));
 }
 
-// Returns flag (0 invisible, 1 visible, 2 out of range) and writes q[4] when visible.
-__device__ __forceinline__ uint32_t clip_int_one(int32_t x0, int32_t y0, int32_t x1, int32_t y1, int4 win,
-                                                 int32_t q[4]) {
-  const int64_t X0 = x0, Y0 = y0, X1 = x1, Y1 = y1;
-  const bool range = (X0 >= -kCoordMax) & (X0 <= kCoordMax) & (Y0 >= -kCoordMax) & (Y0 <= kCoordMax) &
-                     (X1 >= -kCoordMax) & (X1 <= kCoordMax) & (Y1 >= -kCoordMax) & (Y1 <= kCoordMax);
-  if (!range) return 2u;
-  Frac tin{0, 1}, tout{1, 1};
+// Returns flag (0 invisible, 1 visible) and writes q[4] when visible.  I = int64_t for any
+// coordinates in [-2^30, 2^30]; I = int32_t when every coordinate and window bound lies in
+// [-2^14, 2^14] (|w|, den <= 2^15), the common pixel-coordinate case: all 32-bit arithmetic.
+template <typename I>
+__device__ __forceinline__ uint32_t clip_int_core(I X0, I Y0, I X1, I Y1, int4 win, int32_t q[4]) {
+  Frac<I> tin{0, 1}, tout{1, 1};
   bool reject = false;
-  const int64_t w0s[4] = {X0 - win.x, Y0 - win.y, (int64_t)win.z - X0, (int64_t)win.w - Y0};
-  const int64_t w1s[4] = {X1 - win.x, Y1 - win.y, (int64_t)win.z - X1, (int64_t)win.w - Y1};
+  const I w0s[4] = {X0 - (I)win.x, Y0 - (I)win.y, (I)win.z - X0, (I)win.w - Y0};
+  const I w1s[4] = {X1 - (I)win.x, Y1 - (I)win.y, (I)win.z - X1, (I)win.w - Y1};
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const int64_t w0 = w0s[e], w1 = w1s[e];
+    const I w0 = w0s[e], w1 = w1s[e];
     reject |= (w0 < 0) & (w1 < 0);
     if (w0 < 0 && w1 >= 0) {  // entering: alpha = -w0 / (w1 - w0)
-      const Frac a{-w0, w1 - w0};
+      const Frac<I> a{-w0, w1 - w0};
       if (frac_lt(tin, a)) tin = a;
     } else if (w1 < 0 && w0 >= 0) {  // leaving: alpha = w0 / (w0 - w1)
-      const Frac a{w0, w0 - w1};
+      const Frac<I> a{w0, w0 - w1};
       if (frac_lt(a, tout)) tout = a;
     }
   }
   if (reject || frac_lt(tout, tin)) return 0u;
-  const int64_t dx = X1 - X0, dy = Y1 - Y0;
+  const I dx = X1 - X0, dy = Y1 - Y0;
   if (tin.num == 0) {
-    q[0] = x0; q[1] = y0;
+    q[0] = (int32_t)X0; q[1] = (int32_t)Y0;
   } else {
-    const double inv = __drcp_rn((double)tin.den);
+    const auto inv = rcp(tin.den);
     q[0] = lerp_round(X0, dx, tin, inv);
     q[1] = lerp_round(Y0, dy, tin, inv);
   }
   if (tout.num == tout.den) {
-    q[2] = x1; q[3] = y1;
+    q[2] = (int32_t)X1; q[3] = (int32_t)Y1;
   } else {
-    const double inv = __drcp_rn((double)tout.den);
+    const auto inv = rcp(tout.den);
     q[2] = lerp_round(X0, dx, tout, inv);
     q[3] = lerp_round(Y0, dy, tout, inv);
   }
   return 1u;
 }
 
+// Returns flag (0 invisible, 1 visible, 2 out of range) and writes q[4] when visible.
+__device__ __forceinline__ uint32_t clip_int_one(int32_t x0, int32_t y0, int32_t x1, int32_t y1, int4 win,
+                                                 bool small_win, int32_t q[4]) {
+  const uint32_t m = (uint32_t)(x0 + kSmall) | (uint32_t)(y0 + kSmall) | (uint32_t)(x1 + kSmall) |
+                     (uint32_t)(y1 + kSmall);
+  if (small_win && m <= 2u * kSmall) return clip_int_core<int32_t>(x0, y0, x1, y1, win, q);
+  const int64_t X0 = x0, Y0 = y0, X1 = x1, Y1 = y1;
+  const bool range = (X0 >= -kCoordMax) & (X0 <= kCoordMax) & (Y0 >= -kCoordMax) & (Y0 <= kCoordMax) &
+                     (X1 >= -kCoordMax) & (X1 <= kCoordMax) & (Y1 >= -kCoordMax) & (Y1 <= kCoordMax);
+  if (!range) return 2u;
+  return clip_int_core<int64_t>(X0, Y0, X1, Y1, win, q);
+}
+
 __global__ void __launch_bounds__(256) clip_int_kernel(const int32_t* __restrict__ in, int64_t ld_in, int64_t n,
-                                                       int4 win, int32_t* __restrict__ out, int64_t ld_out,
-                                                       uint8_t* __restrict__ flags) {
+                                                       int4 win, bool small_win, int32_t* __restrict__ out,
+                                                       int64_t ld_out, uint8_t* __restrict__ flags) {
   const int64_t ngroups = (n + 3) / 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += stride) {
@@ -106,7 +128,7 @@ __global__ void __launch_bounds__(256) clip_int_kernel(const int32_t* __restrict
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       int32_t q[4];
-      const uint32_t f = clip_int_one(x0[s], y0[s], x1[s], y1[s], win, q);
+      const uint32_t f = clip_int_one(x0[s], y0[s], x1[s], y1[s], win, small_win, q);
 #pragma unroll
       for (int c = 0; c < 4; ++c) o[c][s] = f == 1u ? q[c] : kFill;
       fpack |= f << (8 * s);
@@ -140,7 +162,9 @@ cudaError_t launch_clip_int(const int32_t* in, int64_t ld_in, int64_t n, const i
   const int64_t want = (ngroups + NT - 1) / NT;
   const int64_t cap = (int64_t)device_sm_count() * blocks_per_sm;  // persistent: one resident wave
   const int grid = (int)(want < cap ? want : cap);
-  clip_int_kernel<<<grid, NT, 0, s>>>(in, ld_in, n, make_int4(lo[0], lo[1], hi[0], hi[1]), out, ld_out, flags);
+  const bool small_win = lo[0] >= -kSmall && lo[1] >= -kSmall && hi[0] <= kSmall && hi[1] <= kSmall;
+  clip_int_kernel<<<grid, NT, 0, s>>>(in, ld_in, n, make_int4(lo[0], lo[1], hi[0], hi[1]), small_win, out, ld_out,
+                                      flags);
   return cudaGetLastError();
 }
 

@@ -137,12 +137,20 @@ def int_segments_host(seed, n, mix="screen", ld=None):
     mix "screen": endpoints uniform on [-S/2, 3S/2)^2, S = INT_SCREEN (about 1/4 of each
     endpoint inside); "wide": uniform on [-2^30, 2^30]; "edge": small coordinates around
     the window so endpoints hit edges, corners and ties; "range": "wide" with 1 % of the
-    coordinates pushed outside [-2^30, 2^30] (flag 2).  No clipping arithmetic here."""
+    coordinates pushed outside [-2^30, 2^30] (flag 2); "mixed": each segment "screen" or
+    "wide" with probability 1/2, and 1 % "edge" endpoints beyond +-2^14 (both kernel paths
+    inside one warp).  No clipping arithmetic here."""
     ld = plane_stride(n) if ld is None else ld
     rng = np.random.default_rng(seed)
     out = np.zeros((4, ld), dtype=np.int32)
     if mix == "screen":
         v = rng.integers(-INT_SCREEN // 2, 3 * INT_SCREEN // 2, size=(4, n))
+    elif mix == "mixed":
+        B = 1 << 30
+        v = np.where(rng.random(n) < 0.5, rng.integers(-INT_SCREEN // 2, 3 * INT_SCREEN // 2, size=(4, n)),
+                     rng.integers(-B, B + 1, size=(4, n)))
+        k = 1 << 14
+        v = np.where(rng.random((4, n)) < 0.01, rng.choice(np.array([k, k + 1, -k, -k - 1]), size=(4, n)), v)
     elif mix == "edge":
         v = rng.integers(-3, INT_SCREEN // 512 + 3, size=(4, n)) * 512 + rng.integers(-2, 3, size=(4, n))
     else:

@@ -58,11 +58,11 @@ def test_golden(torch, cs):
 
 
 @pytest.mark.parametrize("n", [1, 3, 4, 5, 31, 1023, 4097, 30001])
-@pytest.mark.parametrize("mix", ["screen", "edge", "wide", "range"])
+@pytest.mark.parametrize("mix", ["screen", "edge", "wide", "range", "mixed"])
 def test_parity(torch, cs, n, mix):
     planes = synth.int_segments_host(1000 + n, n, mix)
     flags = check(torch, cs, planes, n, *SCREEN)
-    if n > 1000 and mix in ("screen", "edge"):
+    if n > 1000 and mix in ("screen", "edge", "mixed"):
         assert (flags == 1).any() and (flags == 0).any()
         if mix == "range":
             assert (flags == 2).any()
@@ -72,6 +72,10 @@ def test_windows(torch, cs):
     B = 1 << 30
     planes = synth.int_segments_host(7, 20000, "wide")
     for lo, hi in (([-B, -B], [B, B]), ([5, 5], [5, 5]), ([-B, 0], [0, B]), ([-1000, -7], [123456, 999999])):
+        check(torch, cs, planes, 20000, lo, hi)
+    k = 1 << 14  # windows at and just past the 32-bit path's bound
+    planes = synth.int_segments_host(8, 20000, "mixed")
+    for lo, hi in (([-k, -k], [k, k]), ([-k - 1, 0], [k, k]), ([0, 0], [k + 1, 5]), ([-k, -k], [-k, -k])):
         check(torch, cs, planes, 20000, lo, hi)
 
 
