@@ -119,10 +119,15 @@ __device__ __forceinline__ uint32_t clip_int_small(int32_t X0, int32_t Y0, int32
   }
   const uint32_t vis = !reject & !(out_n * in_d < in_n * out_d);
   const int32_t dx = X1 - X0, dy = Y1 - Y0;
-  const float inv_in = __frcp_rn((float)in_d), inv_out = __frcp_rn((float)out_d);
+  // inv = MUFU.RCP (relative error < 2^-22): the estimate stays within 1.5 * 2^-22 * 2^15 < 1
+  // of d num / den, so one remainder fix still suffices (the correctly rounded __frcp_rn is a
+  // ~10-instruction Newton sequence with a slow-path branch).
+  float inv_in, inv_out;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv_in) : "f"((float)in_d));
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv_out) : "f"((float)out_d));
   auto lerp = [](int32_t p, int32_t d, int32_t num, int32_t den, float inv) {
     const int32_t x = d * num;
-    int32_t qq = (int32_t)floorf(__fmul_rn((float)x, inv));
+    int32_t qq = __float2int_rd(__fmul_rn((float)x, inv));
     int32_t r = x - qq * den;
     qq += (r >= den) - (r < 0);
     r += (r < 0 ? den : 0) - (r >= den ? den : 0);
