@@ -85,12 +85,26 @@ MUTANTS += [
     ("K6 survivor keeps the smaller id", "cluster_oracle.py",
      "pairs = [(r, s) for r, s in best.items() if s is not None and r < s and best.get(s) == r]",
      "pairs = [(s, r) for r, s in best.items() if s is not None and r < s and best.get(s) == r]", "killed"),
+    ("M0 unmutated (harness check)", "int_oracle.py", "import numpy as np", "import numpy as np", "equivalent"),
+    ("I1 round half down", "int_oracle.py", "math.floor(x + Fraction(1, 2))", "math.ceil(x - Fraction(1, 2))", "killed"),
+    ("I2 truncate instead of round", "int_oracle.py", "math.floor(x + Fraction(1, 2))", "int(x)", "killed"),
+    ("I3 WEC sign on the lo edge", "int_oracle.py", "(p0[k] - lo[k], p1[k] - lo[k])", "(lo[k] - p0[k], lo[k] - p1[k])",
+     "killed"),
+    ("I4 max as min for t_in", "int_oracle.py", "t_in = max(t_in, Fraction(w0, w0 - w1))",
+     "t_in = min(t_in, Fraction(w0, w0 - w1))", "killed"),
+    ("I5 open window", "int_oracle.py", "if t_in > t_out:", "if t_in >= t_out:", "killed"),
+    ("I6 Q1 from t_in", "int_oracle.py", "q1 = tuple(int(p0[k]) + round_half_up(d[k] * t_out)",
+     "q1 = tuple(int(p0[k]) + round_half_up(d[k] * t_in)", "killed"),
+    ("I7 range bound 2^31", "int_oracle.py", "COORD_MAX = 1 << 30", "COORD_MAX = 1 << 31", "killed"),
+    ("I8 swapped axes in d", "int_oracle.py", "d = (p1[0] - p0[0], p1[1] - p0[1])", "d = (p1[1] - p0[1], p1[0] - p0[0])",
+     "killed"),
 ]
 
 TESTS = {"clip_oracle_impl.h": ["tests/test_oracle_pins.py", "tests/test_oracle_homog.py"],
          "clip_homog_impl.h": ["tests/test_oracle_homog.py"],
          "tof_oracle.py": ["tests/test_oracle_tof.py"],
-         "cluster_oracle.py": ["tests/test_oracle_cluster.py"]}
+         "cluster_oracle.py": ["tests/test_oracle_cluster.py"],
+         "int_oracle.py": ["tests/test_oracle_int.py"]}
 
 
 def run_python_mutant(fname, orig, mut):
@@ -110,12 +124,12 @@ def run_python_mutant(fname, orig, mut):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", choices=["cuboid", "homog", "python"])
+    ap.add_argument("--only", choices=["cuboid", "homog", "python", "int"])
     a = ap.parse_args()
     rows, bad = [], 0
     for mid, fname, orig, mut, expect in MUTANTS:
         if (a.only == "cuboid" and fname != "clip_oracle_impl.h" or a.only == "homog" and fname != "clip_homog_impl.h"
-                or a.only == "python" and not fname.endswith(".py")):
+                or a.only == "python" and not fname.endswith(".py") or a.only == "int" and fname != "int_oracle.py"):
             continue
         if fname.endswith(".py"):
             got = "killed" if run_python_mutant(fname, orig, mut) else "survived"
