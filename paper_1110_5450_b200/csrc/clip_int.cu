@@ -35,9 +35,7 @@ template <typename I>
 __device__ __forceinline__ bool frac_lt(Frac<I> a, Frac<I> b) { return a.num * b.den < b.num * a.den; }
 
 __device__ __forceinline__ double est_quot(int64_t x, double inv) { return floor(__dmul_rn((double)x, inv)); }
-__device__ __forceinline__ float est_quot(int32_t x, float inv) { return floorf(__fmul_rn((float)x, inv)); }
 __device__ __forceinline__ double rcp(int64_t d) { return __drcp_rn((double)d); }
-__device__ __forceinline__ float rcp(int32_t d) { return __frcp_rn((float)d); }
 
 // p + round_half_up(d * t): q = floor(d num / den), r = d num - q den in [0, den); +1 when
 // 2r >= den.  No integer division (64-bit division is a ~70-instruction software routine that
@@ -100,21 +98,28 @@ __device__ __forceinline__ uint32_t clip_int_core(I X0, I Y0, I X1, I Y1, int4 w
 // t = 0 and t = 1 need no special case since lerp_round then returns p and p + d exactly.
 __device__ __forceinline__ uint32_t clip_int_small(int32_t X0, int32_t Y0, int32_t X1, int32_t Y1, int4 win,
                                                    int32_t q[4]) {
+  // Per axis, the sign of d decides which edge can be entered and which left (lo / hi for
+  // d > 0, hi / lo for d < 0), and both alphas share the denominator |d| = w0 - w1: one
+  // entering and one leaving candidate per axis instead of both tests on all four edges.
+  // A d = 0 axis never yields a candidate unless the segment is rejected on it.
   int32_t in_n = 0, in_d = 1, out_n = 1, out_d = 1;
   bool reject = false;
-  const int32_t w0s[4] = {X0 - win.x, Y0 - win.y, win.z - X0, win.w - Y0};
-  const int32_t w1s[4] = {X1 - win.x, Y1 - win.y, win.z - X1, win.w - Y1};
+  const int32_t p0s[2] = {X0, Y0}, p1s[2] = {X1, Y1}, los[2] = {win.x, win.y}, his[2] = {win.z, win.w};
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const int32_t w0 = w0s[e], w1 = w1s[e];
-    reject |= (w0 < 0) & (w1 < 0);
-    const bool ent = (w0 < 0) & (w1 >= 0), lea = (w1 < 0) & (w0 >= 0);
-    const int32_t an = ent ? -w0 : w0, ad = ent ? w1 - w0 : w0 - w1;
-    const bool up_in = ent & (in_n * ad < an * in_d);
-    const bool up_out = lea & (an * out_d < out_n * ad);
-    in_n = up_in ? an : in_n;
+  for (int k = 0; k < 2; ++k) {
+    const int32_t p0 = p0s[k], p1 = p1s[k], lo = los[k], hi = his[k];
+    reject |= ((p0 < lo) & (p1 < lo)) | ((p0 > hi) & (p1 > hi));
+    const int32_t d = p1 - p0;
+    const bool pos = d > 0;
+    const int32_t ad = pos ? d : -d;
+    const int32_t en = pos ? lo - p0 : p0 - hi;  // entering alpha = en / ad when en > 0
+    const int32_t ln = pos ? hi - p0 : p0 - lo;  // leaving alpha = ln / ad
+    const bool lea = pos ? p1 > hi : p1 < lo;
+    const bool up_in = (en > 0) & (in_n * ad < en * in_d);
+    const bool up_out = lea & (ln * out_d < out_n * ad);
+    in_n = up_in ? en : in_n;
     in_d = up_in ? ad : in_d;
-    out_n = up_out ? an : out_n;
+    out_n = up_out ? ln : out_n;
     out_d = up_out ? ad : out_d;
   }
   const uint32_t vis = !reject & !(out_n * in_d < in_n * out_d);
