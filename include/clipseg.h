@@ -64,7 +64,8 @@ const char* clip_status_string(int status);
  * in:    2*dim planes (ld_in), n segments.
  * out:   2*dim planes (ld_out); row i = clipped Q0,Q1 of segment i if visible, else the
  *        canonical quiet NaN (0x7FC00000 / 0x7FF8000000000000) in every plane.
- *        out == in (same ld) is allowed: each thread reads its segments before writing.
+ *        out == in (same ld) is allowed: each thread reads its segments before writing;
+ *        any other overlap of out with in -> CLIP_EINVAL.
  * flags: n bytes (nullable): 1 visible, 0 invisible. */
 int clip_segments_f32(const float* in, int64_t ld_in, int64_t n, const clip_window_f32* win,
                       float* out, int64_t ld_out, uint8_t* flags, void* stream);
@@ -195,7 +196,8 @@ int clip_cluster_frames(const float* z, const float* phi, const uint8_t* valid, 
  * I4 Q_e,k = P0_k + floor(d_k t_e + 1/2) (round half up, exact);
  * I5 invisible rows hold INT32_MIN in all 4 planes; I6 flag 2 = a coordinate outside I1.
  * in, out: 4 int32 planes x0, y0, x1, y1 (ld_in / ld_out, same layout and alignment rules
- *          as the float calls; out == in allowed).
+ *          as the float calls; out == in with ld_out == ld_in allowed, any other overlap
+ *          -> CLIP_EINVAL).
  * flags:   (nullable, 4-byte aligned) n bytes: 1 visible, 0 invisible, 2 out of range.
  * win:     host pointer; lo > hi or a bound outside [-2^30, 2^30] -> CLIP_EINVAL.
  * Results are bit-identical to the exact-rational oracle (oracle/int_oracle.py). */

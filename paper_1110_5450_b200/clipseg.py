@@ -282,13 +282,18 @@ def clip_int(planes, n, lo, hi, out=None, flags=None, want_flags=True, stream=No
     """planes: CUDA int32 (4, ld) x0, y0, x1, y1 (ld a multiple of 4, >= n); lo, hi: 2 ints.
     Returns (out int32 (4, ld_out), flags uint8[n] or None)."""
     torch = _torch()
-    ld = planes.shape[1]
     if out is None:
         out = torch.empty_like(planes)
+    for name, t in (("planes", planes), ("out", out)):
+        if t.dtype != torch.int32:
+            raise TypeError(f"clip_int: {name} must be int32, got {t.dtype}")
+        if t.dim() != 2 or t.shape[0] != 4 or t.stride(1) != 1:
+            raise ValueError(f"clip_int: {name} must be a (4, ld) row-major plane view with unit inner stride")
     if flags is None and want_flags:
         flags = torch.empty(max(n, 4), dtype=torch.uint8, device=planes.device)
     win = clip_window_i32((ctypes.c_int32 * 2)(*lo), (ctypes.c_int32 * 2)(*hi))
-    _check(clip_segments_i32(planes.data_ptr(), ld, n, ctypes.byref(win), out.data_ptr(), out.shape[1],
+    # the plane strides are the views' row strides (a column slice big[:, :m] keeps big's ld)
+    _check(clip_segments_i32(planes.data_ptr(), planes.stride(0), n, ctypes.byref(win), out.data_ptr(), out.stride(0),
                              flags.data_ptr() if flags is not None else None, _stream(stream)),
            "clip_segments_i32")
     return out, flags

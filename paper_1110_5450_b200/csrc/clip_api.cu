@@ -52,6 +52,19 @@ Window<T, D> to_window(const typename WinT<T>::type* win) {
   return w;
 }
 
+// Byte extent of `planes` planes of `ld` elements holding n rows each.
+inline int64_t plane_bytes(int planes, int64_t ld, int64_t n, size_t esz) {
+  return ((int64_t)(planes - 1) * ld + n) * (int64_t)esz;
+}
+// Element-wise (dense) kernels read a thread's rows before writing them, so in place
+// (out == in with the same plane stride) is allowed; any other overlap would let one thread's
+// stores race with another's loads.
+inline bool overlap_ok(const void* in, int64_t in_bytes, const void* out, int64_t out_bytes, bool same_ld) {
+  const char *ib = reinterpret_cast<const char*>(in), *ob = reinterpret_cast<const char*>(out);
+  if (ib == ob) return same_ld;
+  return !(ob < ib + in_bytes && ib < ob + out_bytes);
+}
+
 int status_of(cudaError_t e) { return e == cudaSuccess ? CLIP_OK : CLIP_ECUDA; }
 
 template <typename T>
@@ -63,6 +76,10 @@ int dense(const T* in, int64_t ld_in, int64_t n, const typename WinT<T>::type* w
   if (n == 0) return CLIP_OK;
   if ((st = check_planes(in, ld_in, n)) || (st = check_planes(out, ld_out, n))) return st;
   if (flags && !aligned(flags, 4)) return CLIP_EALIGN;
+  const int planes = 2 * win->dim;
+  if (!overlap_ok(in, plane_bytes(planes, ld_in, n, sizeof(T)), out, plane_bytes(planes, ld_out, n, sizeof(T)),
+                  ld_in == ld_out))
+    return CLIP_EINVAL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (win->dim == 2)
     return status_of(launch_dense<T, BoxOp<T, 2>>(in, ld_in, n, to_window<T, 2>(win), out, ld_out, flags, s));
@@ -107,6 +124,9 @@ int homog_dense(const T* in, int64_t ld_in, int64_t n, int ndc, T* out, int64_t 
   int st;
   if ((st = check_planes(in, ld_in, n)) || (st = check_planes(out, ld_out, n))) return st;
   if (flags && !aligned(flags, 4)) return CLIP_EALIGN;
+  if (!overlap_ok(in, plane_bytes(8, ld_in, n, sizeof(T)), out, plane_bytes(ndc ? 6 : 8, ld_out, n, sizeof(T)),
+                  ld_in == ld_out))
+    return CLIP_EINVAL;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const NoParams none{0};
   if (ndc) return status_of(launch_dense<T, HomogOp<T, true>>(in, ld_in, n, none, out, ld_out, flags, s));
@@ -350,6 +370,8 @@ int clip_segments_i32(const int32_t* in, int64_t ld_in, int64_t n, const clip_wi
   int st;
   if ((st = check_planes(in, ld_in, n)) || (st = check_planes(out, ld_out, n))) return st;
   if (flags && !aligned(flags, 4)) return CLIP_EALIGN;
+  if (!overlap_ok(in, plane_bytes(4, ld_in, n, 4), out, plane_bytes(4, ld_out, n, 4), ld_in == ld_out))
+    return CLIP_EINVAL;
   return status_of(launch_clip_int(in, ld_in, n, win->lo, win->hi, out, ld_out, flags,
                                    reinterpret_cast<cudaStream_t>(stream)));
 }

@@ -148,8 +148,10 @@ __device__ __forceinline__ uint32_t clip_int_small(int32_t X0, int32_t Y0, int32
 // Returns flag (0 invisible, 1 visible, 2 out of range) and writes q[4] when visible.
 __device__ __forceinline__ uint32_t clip_int_one(int32_t x0, int32_t y0, int32_t x1, int32_t y1, int4 win,
                                                  bool small_win, int32_t q[4]) {
-  const uint32_t m = (uint32_t)(x0 + kSmall) | (uint32_t)(y0 + kSmall) | (uint32_t)(x1 + kSmall) |
-                     (uint32_t)(y1 + kSmall);
+  // biased in unsigned arithmetic (no signed overflow near INT32_MAX): every coordinate lies in
+  // [-2^14, 2^14] iff the largest biased value is <= 2^15
+  const uint32_t m = max(max((uint32_t)x0 + (uint32_t)kSmall, (uint32_t)y0 + (uint32_t)kSmall),
+                         max((uint32_t)x1 + (uint32_t)kSmall, (uint32_t)y1 + (uint32_t)kSmall));
   if (small_win && m <= 2u * kSmall) return clip_int_small(x0, y0, x1, y1, win, q);
   const int64_t X0 = x0, Y0 = y0, X1 = x1, Y1 = y1;
   const bool range = (X0 >= -kCoordMax) & (X0 <= kCoordMax) & (Y0 >= -kCoordMax) & (Y0 <= kCoordMax) &
@@ -158,8 +160,10 @@ __device__ __forceinline__ uint32_t clip_int_one(int32_t x0, int32_t y0, int32_t
   return clip_int_core<int64_t>(X0, Y0, X1, Y1, win, q);
 }
 
-__global__ void __launch_bounds__(256) clip_int_kernel(const int32_t* __restrict__ in, int64_t ld_in, int64_t n,
-                                                       int4 win, bool small_win, int32_t* __restrict__ out,
+// in and out may be the same buffer (out == in, ld_out == ld_in: each thread reads its rows
+// before writing them), so neither is __restrict__.
+__global__ void __launch_bounds__(256) clip_int_kernel(const int32_t* in, int64_t ld_in, int64_t n,
+                                                       int4 win, bool small_win, int32_t* out,
                                                        int64_t ld_out, uint8_t* __restrict__ flags) {
   const int64_t ngroups = (n + 3) / 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
