@@ -80,7 +80,11 @@ int clip_segments_f64(const double* in, int64_t ld_in, int64_t n, const clip_win
  * flags:     (nullable) n bytes, as in the dense call.
  * d_count:   one int64 in device memory receiving count (the caller synchronises).
  * workspace: device scratch of clip_compact_workspace_bytes(n) bytes (tile-claim counter
- *            and per-tile look-back status words); reset by the call itself. */
+ *            and per-tile look-back status words).  It must be ZERO-FILLED before its first
+ *            use (e.g. cudaMemsetAsync); every successful call leaves it zero-filled again,
+ *            so one workspace serves any number of calls issued in order on one stream and
+ *            a call is a single kernel launch (no per-call memset).  Calls that may run
+ *            concurrently need distinct workspaces.  After a failed call, zero it again. */
 size_t clip_compact_workspace_bytes(int64_t n);
 int clip_segments_compact_f32(const float* in, int64_t ld_in, int64_t n, const clip_window_f32* win,
                               float* out, int64_t ld_out, int64_t* out_index, int64_t index_base,

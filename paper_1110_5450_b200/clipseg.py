@@ -185,7 +185,8 @@ class CompactBuffers:
         self.n, self.dim = n, dim
         self.out = empty_planes(n, dim, dtype, device)
         self.count = torch.zeros(1, dtype=torch.int64, device=device)
-        self.ws = torch.empty(max(int(clip_compact_workspace_bytes(n)), 128), dtype=torch.uint8, device=device)
+        # zero-filled once; every call leaves it zero-filled again (include/clipseg.h)
+        self.ws = torch.zeros(max(int(clip_compact_workspace_bytes(n)), 128), dtype=torch.uint8, device=device)
         self.index = torch.empty(max(n, 1), dtype=torch.int64, device=device) if with_index else None
         self.flags = torch.empty(max(n, 1), dtype=torch.uint8, device=device) if with_flags else None
 

@@ -235,6 +235,10 @@ int compact_host(const T* h_in, int64_t ld_in, int64_t n, const typename WinT<T>
     return cudaEventRecord(comp_done[s], sc) == cudaSuccess;
   };
 
+  // the compacting kernel needs a zero-filled workspace on first use and leaves it zero:
+  // clear both sets' workspaces once per call (the staging buffer is the caller's)
+  for (int s = 0; s < 2 && ok; ++s)
+    ok = cudaMemsetAsync(set_ptr(s, L.ws_off), 0, clip_compact_workspace_bytes(chunk), sc) == cudaSuccess;
   if (ok) ok = issue(0);
   for (int64_t j = 0; ok && j < nch; ++j) {
     const int s = (int)(j & 1);

@@ -103,6 +103,19 @@ __device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// One thread's shared-memory fetch-and-add (atomicAdd would wrap it in warp-aggregation code
+// for a single active lane).
+__device__ __forceinline__ int atom_add_shared(int* p, int v) {
+  int old;
+  asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_addr(p)), "r"(v) : "memory");
+  return old;
+}
+// One thread's global 64-bit fetch-and-add (relaxed, gpu scope).
+__device__ __forceinline__ unsigned long long atom_add_global(unsigned long long* p, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.relaxed.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
 }
@@ -122,6 +135,34 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
       "r"(parity), "r"(1000000u)
       : "memory");
+}
+
+// The same on 32-bit shared addresses computed once (no generic-to-shared conversion in the
+// hot loop).
+__device__ __forceinline__ void mbar_arrive_a(uint32_t a) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_a(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+
+// Non-blocking: has the phase with the given parity completed?
+__device__ __forceinline__ bool mbar_test_a(uint32_t a, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(done)
+      : "r"(a), "r"(parity)
+      : "memory");
+  return done != 0;
 }
 
 // Low-duty-cycle wait for the scan warp, which waits most of its life: a non-blocking phase
@@ -192,6 +233,76 @@ __device__ __noinline__ void global_scanner(unsigned long long* status, int64_t 
     base += ready;
   }
   if (lane == 0) *d_count = (int64_t)running;
+}
+
+// A block's scan warp: for each of the block's tiles in claim order, once its compute warps'
+// NSUB counts are in (mb_cnt), exclusive-prefix them, wait for the scanner's inclusive prefix
+// of the tile and hand the offsets over (mb_pre).  It then zeroes the tile's status word: the
+// scanner never reads a word again once it holds the prefix, so the workspace is all zero
+// again when the launch ends and the next call needs no memset.
+// s_tileof (nullable): receives each iteration's tile id in its slot, for consumers that
+// outlive the tile ring.
+template <int NSUB, int NBUF>
+__device__ __forceinline__ void tile_scan_warp(int lane, int64_t ntiles, unsigned long long* status,
+                                               const int64_t* s_tile, const int (*s_cnt)[NSUB], int (*s_pre)[NSUB],
+                                               int64_t* s_prefix, int* s_done, uint64_t* mb_tile, uint64_t* mb_cnt,
+                                               uint64_t* mb_pre, int64_t* s_tileof = nullptr) {
+  static_assert(NSUB <= 64, "two counts per lane");
+  int b = 0;
+  unsigned par = 0;  // bit q: parity of the next phase of mb_cnt[q] / mb_pre[q]
+  for (int64_t k = 0;; ++k) {
+    mbar_wait_sleepy(&mb_tile[k & kRingMask], (uint32_t)((k / kTileRing) & 1), CLIPSEG_SCAN_SLEEP_NS);
+    const int64_t tile = s_tile[k & kRingMask];
+    if (tile >= ntiles) break;
+    mbar_wait_sleepy(&mb_cnt[b], (par >> b) & 1u, CLIPSEG_SCAN_SLEEP_NS);  // the compute warps' counts of tile k
+    // lane holds counts lane and lane + 32, packed in the low / high 16 bits (a tile count
+    // is below 2^16)
+    const int c0 = (lane < NSUB) ? s_cnt[b][lane] : 0;
+    const int c1 = (NSUB > 32 && lane + 32 < NSUB) ? s_cnt[b][lane + 32] : 0;
+    const int c = c0 | (c1 << 16);
+    int incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    const int tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    if (lane < NSUB) s_pre[b][lane] = (incl & 0xFFFF) - c0;
+    if (NSUB > 32 && lane + 32 < NSUB) s_pre[b][lane + 32] = (tot & 0xFFFF) + (incl >> 16) - c1;
+    const int64_t total = (tot & 0xFFFF) + (tot >> 16);
+    if (lane == 0) {
+      CLIP_TRACE(tile, 3, trace_now());
+      unsigned long long st;
+      while (((st = ld_relaxed(status + tile)) >> 62) != 2u)  // the scanner's inclusive prefix
+        __nanosleep(CLIPSEG_POLL_NS);  // it typically lands several microseconds after the aggregate
+      CLIP_TRACE(tile, 4, trace_now());
+      CLIP_TRACE(tile, 7, blockIdx.x);
+      st_relaxed(status + tile, 0ull);  // consumed: leave the word clean for the next call
+      s_prefix[b] = (int64_t)(st & kValueMask) - total;
+      s_done[b] = 0;
+      if (s_tileof) s_tileof[b] = tile;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&mb_pre[b]);  // tile k's offsets published
+    par ^= 1u << b;
+    b = (b + 1 == NBUF) ? 0 : b + 1;
+  }
+}
+
+// Workspace header: [0] tile-claim counter, [1] finished-block counter.  The last block of
+// the grid to finish resets both, so (with the status words zeroed by the scan warps) the
+// workspace is all zero after every launch.  Called by one warp per block, after every other
+// warp of the block has stopped touching the workspace (the scan warp is the block's last
+// user: compute warps do not exit before their final copy-out, which waits on the scan warp).
+__device__ __forceinline__ void block_exit(unsigned long long* ws, int lane) {
+  if (lane == 0) {
+    __threadfence();
+    const unsigned long long done = atomicAdd(ws + 1, 1ull);
+    if (done == (unsigned long long)gridDim.x - 1) {
+      ws[0] = 0ull;
+      ws[1] = 0ull;
+    }
+  }
 }
 
 }  // namespace
@@ -269,49 +380,16 @@ __global__ void __launch_bounds__(CompactShape<T, Op, INDEX>::kThreads, CompactS
   }
   __syncthreads();
   if (blockIdx.x == 0) {  // block 0 only scans; it processes no tiles
-    if (warp == kComputeWarps) global_scanner(status, ntiles, lane, d_count);
+    if (warp == kComputeWarps) {
+      global_scanner(status, ntiles, lane, d_count);
+      block_exit(ws, lane);
+    }
     return;
   }
 
   if (warp == kComputeWarps) {
-    // ------------------------------------------------------------------ scan warp
-    int b = 0;
-    unsigned par = 0;  // bit q: parity of the next phase of mb_cnt[q] / mb_pre[q]
-    for (int64_t k = 0;; ++k) {
-      mbar_wait_sleepy(&mb_tile[k & kRingMask], (uint32_t)((k / kTileRing) & 1), CLIPSEG_SCAN_SLEEP_NS);
-      const int64_t tile = s_tile[k & kRingMask];
-      if (tile >= ntiles) break;
-      mbar_wait_sleepy(&mb_cnt[b], (par >> b) & 1u, CLIPSEG_SCAN_SLEEP_NS);  // the compute warps' counts of tile k
-      // lane holds sub-tiles lane and lane + 32, packed in the low / high 16 bits (a tile
-      // count is at most 32 x 128 < 2^16)
-      const int c0 = (lane < NSUB) ? s_cnt[b][lane] : 0;
-      const int c1 = (NSUB > 32 && lane + 32 < NSUB) ? s_cnt[b][lane + 32] : 0;
-      const int c = c0 | (c1 << 16);
-      int incl = c;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-        if (lane >= d) incl += y;
-      }
-      const int tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
-      if (lane < NSUB) s_pre[b][lane] = (incl & 0xFFFF) - c0;
-      if (NSUB > 32 && lane + 32 < NSUB) s_pre[b][lane + 32] = (tot & 0xFFFF) + (incl >> 16) - c1;
-      const int64_t total = (tot & 0xFFFF) + (tot >> 16);
-      if (lane == 0) {
-        CLIP_TRACE(tile, 3, trace_now());
-        unsigned long long st;
-        while (((st = ld_relaxed(status + tile)) >> 62) != 2u)  // the scanner's inclusive prefix
-          __nanosleep(CLIPSEG_POLL_NS);  // it typically lands several microseconds after the aggregate
-        CLIP_TRACE(tile, 4, trace_now());
-        CLIP_TRACE(tile, 7, blockIdx.x);
-        s_prefix[b] = (int64_t)(st & kValueMask) - total;
-        s_done[b] = 0;
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&mb_pre[b]);  // tile k's offsets published
-      par ^= 1u << b;
-      b = (b + 1 == NBUF) ? 0 : b + 1;
-    }
+    tile_scan_warp<NSUB, NBUF>(lane, ntiles, status, s_tile, s_cnt, s_pre, s_prefix, s_done, mb_tile, mb_cnt, mb_pre);
+    block_exit(ws, lane);
     return;
   }
 
@@ -566,37 +644,473 @@ __global__ void __launch_bounds__(CompactShape<T, Op, INDEX>::kThreads, CompactS
   }
 }
 
+// ======================================================================================
+// Packed variant (the headline 2D fp32 instantiation).  Same grid organisation as above
+// (block 0 = global scanner; per block: compute warps + scan warp, dynamic tile claims,
+// NBUF staged tiles, copy-out NBUF-1 tiles after the compute), but a compute warp owns a
+// contiguous BATCH = PW x 128 segments of each tile and works on it in two phases:
+//
+//  1. R3 only (Op::keep) on its PW register-held sub-tiles; the kept segments are written,
+//     in segment order, as rows of an array-of-structures list at the front of the warp's
+//     staging region (plus their local indices), so the segments R3 rejects — about 40 % of
+//     the headline workload — are never clipped.  The next tile's batch is then loaded
+//     into the same registers, in flight during phase 2;
+//  2. the kept rows are clipped 32 at a time, one per lane (Op::clip_one); ballot + popc
+//     rank the visible ones and each is written back, as a row, at its rank in the same
+//     region (rank <= list position, so the rows still to be read are never overwritten).
+//
+// The region then holds the batch's visible rows contiguously; NBUF-1 tiles later the warp
+// copies them to their global rows (one shared-memory row load + 2·D coalesced stores per
+// row, only ceil(count/32) rounds).  Flags go through a per-warp byte array (zeroed in
+// phase 1, the visible ones set in phase 2, stored as words).
+template <typename T, class Op, bool INDEX> struct PackedShape {
+  static constexpr PackedKnobs K = packed_knobs<T, Op>();
+  static constexpr int IN = Op::IN, OUT = Op::OUT;
+  static constexpr int V = Vec16<T>::N;  // segments per 128-bit vector
+  static constexpr int SUB = 32 * V;     // segments per sub-tile (one vector per plane per lane)
+  static constexpr int PW = K.pw;        // sub-tiles per warp batch
+  static constexpr int BATCH = PW * SUB; // segments per warp batch (local indices are bytes)
+  static constexpr int W = K.warps;      // compute warps
+  static constexpr int BT = W * BATCH;   // segments per block tile
+  static constexpr int NBUF = K.nbuf;    // staged tiles (the copy-out lags NBUF-1 tiles)
+  static constexpr size_t ROWB = (size_t)IN * sizeof(T);
+  static constexpr size_t kRegion = (size_t)BATCH * IN;               // elements per warp region
+  static constexpr size_t kStageBytes = (size_t)NBUF * W * kRegion * sizeof(T);
+  static constexpr size_t kIdxOff = kStageBytes;                      // [W][BATCH] list -> local index
+  static constexpr size_t kFlagOff = kIdxOff + (size_t)W * BATCH;     // [W][BATCH] flag bytes
+  static constexpr size_t kLixOff = kFlagOff + (size_t)W * BATCH;     // [NBUF][W][BATCH] staged indices
+  static constexpr size_t kSmemBytes = kLixOff + (INDEX ? (size_t)NBUF * W * BATCH : 0);
+  static constexpr int kThreads = (W + 1) * 32;
+  static_assert(BATCH <= 256, "local indices are bytes");
+  static_assert(OUT <= IN, "rows are written back in place");
+  static_assert(kSmemBytes <= kMaxSmemPerBlock, "shared memory");
+  static_assert(BT >= kMinCompactTile, "workspace sizing");
+};
+
+// Shared memory by 32-bit shared-window address (computed once per kernel, so the hot loops
+// carry no generic-to-shared conversions).  Rows of N elements, aligned to 16 B (fp32 rows
+// of 4 or 8, fp64 rows) or 8 B (fp32 rows of 6).
+__device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_u32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
+}
+template <typename T, int N>
+__device__ __forceinline__ void sts_row(uint32_t a, const T (&v)[N]) {
+  if constexpr (sizeof(T) == 4) {
+    static_assert(N % 2 == 0, "row layout");
+#pragma unroll
+    for (int i = 0; i + 4 <= N; i += 4)
+      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a + 4 * i), "f"(v[i]), "f"(v[i + 1]),
+                   "f"(v[i + 2]), "f"(v[i + 3])
+                   : "memory");
+    if constexpr (N % 4 == 2)
+      asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a + 4 * (N - 2)), "f"(v[N - 2]), "f"(v[N - 1]) : "memory");
+  } else {
+    static_assert(N % 2 == 0, "row layout");
+#pragma unroll
+    for (int i = 0; i < N; i += 2)
+      asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(a + 8 * i), "d"(v[i]), "d"(v[i + 1]) : "memory");
+  }
+}
+template <typename T, int N>
+__device__ __forceinline__ void lds_row(uint32_t a, T (&v)[N]) {
+  if constexpr (sizeof(T) == 4) {
+#pragma unroll
+    for (int i = 0; i + 4 <= N; i += 4)
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(v[i]), "=f"(v[i + 1]), "=f"(v[i + 2]), "=f"(v[i + 3])
+                   : "r"(a + 4 * i)
+                   : "memory");
+    if constexpr (N % 4 == 2)
+      asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v[N - 2]), "=f"(v[N - 1]) : "r"(a + 4 * (N - 2)) : "memory");
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; i += 2)
+      asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v[i]), "=d"(v[i + 1]) : "r"(a + 8 * i) : "memory");
+  }
+}
+
+#ifndef CLIPSEG_PK_MAXNREG
+#define CLIPSEG_PK_MAXNREG 0  // > 0: register cap instead of the launch bounds (A/B builds)
+#endif
+#if CLIPSEG_PK_MAXNREG > 0
+#define CLIPSEG_PK_BOUNDS(...) __maxnreg__(CLIPSEG_PK_MAXNREG)
+#else
+#define CLIPSEG_PK_BOUNDS(...) __launch_bounds__(__VA_ARGS__, 1)
+#endif
 template <typename T, class Op, bool FLAGS, bool INDEX>
-static cudaError_t launch_compact_variant(const T* in, int64_t ld_in, int64_t n, const typename Op::Params& w, T* out,
+__global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_compact_packed_kernel(
+    const T* __restrict__ in, int64_t ld_in, int64_t n, typename Op::Params w, T* __restrict__ out, int64_t ld_out,
+    int64_t* __restrict__ out_index, int64_t index_base, uint8_t* __restrict__ flags, int64_t* __restrict__ d_count,
+    unsigned long long* __restrict__ ws, int64_t ntiles) {
+  typedef PackedShape<T, Op, INDEX> S;
+  constexpr int IN = S::IN, OUT = S::OUT, V = S::V, SUB = S::SUB, PW = S::PW, BATCH = S::BATCH, W = S::W;
+  constexpr int BT = S::BT, NBUF = S::NBUF;
+  constexpr uint32_t ROWB = (uint32_t)S::ROWB;  // staged row bytes (list rows and output rows)
+  static_assert(NBUF >= 2 && NBUF <= kTileRing - 3, "tile ring");
+
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int s_cnt[NBUF][W], s_pre[NBUF][W];
+  __shared__ int64_t s_prefix[NBUF];
+  __shared__ int s_done[NBUF];
+  __shared__ int64_t s_tile[kTileRing];
+  __shared__ __align__(8) uint64_t mb_cnt[NBUF];
+  __shared__ __align__(8) uint64_t mb_pre[NBUF];
+  __shared__ __align__(8) uint64_t mb_tile[kTileRing];
+
+  unsigned long long* counter = ws;
+  unsigned long long* status = ws + kWsHeaderBytes / 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < NBUF; ++q) {
+      s_done[q] = 0;
+      mbar_init(&mb_cnt[q], W);
+      mbar_init(&mb_pre[q], 1);
+    }
+    for (int q = 0; q < kTileRing; ++q) mbar_init(&mb_tile[q], 1);
+    if (blockIdx.x != 0) {  // the tiles of iterations 0 and 1
+      s_tile[0] = (int64_t)atom_add_global(counter, 1ull);
+      s_tile[1] = (int64_t)atom_add_global(counter, 1ull);
+      mbar_arrive(&mb_tile[0]);
+      mbar_arrive(&mb_tile[1]);
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0) {
+    if (warp == W) {
+      global_scanner(status, ntiles, lane, d_count);
+      block_exit(ws, lane);
+    }
+    return;
+  }
+  if (warp == W) {
+    tile_scan_warp<W, NBUF>(lane, ntiles, status, s_tile, s_cnt, s_pre, s_prefix, s_done, mb_tile, mb_cnt, mb_pre);
+    block_exit(ws, lane);
+    return;
+  }
+
+  // ------------------------------------------------------------------ compute warps
+  const typename Op::KeepParams kparams = Op::keep_params(w);
+  const uint32_t sbase = smem_addr(smem_raw);
+  const uint32_t lidx_a = sbase + (uint32_t)S::kIdxOff + warp * BATCH;    // list position -> local index
+  const uint32_t lflag_a = sbase + (uint32_t)S::kFlagOff + warp * BATCH;  // local index -> flag
+  const uint32_t mbt_a = smem_addr(mb_tile), mbc_a = smem_addr(mb_cnt), mbp_a = smem_addr(mb_pre);
+  const unsigned lt_mask = (1u << lane) - 1u;
+  const int64_t full_tiles = n / BT;  // tiles whose every batch is full
+  const T* lane_in = in + (int64_t)warp * BATCH + lane * V;
+  auto region_of = [&](int buf) -> uint32_t {
+    return sbase + (uint32_t)(((size_t)buf * W + warp) * S::kRegion * sizeof(T));
+  };
+  // segments of this warp's batch of tile t before the end of the input (BATCH when full)
+  auto batch_rem = [&](int64_t t) -> int {
+    if (t < full_tiles) return BATCH;
+    const int64_t r = n - (t * BT + (int64_t)warp * BATCH);
+    return r >= BATCH ? BATCH : (r > 0 ? (int)r : 0);
+  };
+  T cur[PW][IN][V];
+  auto load = [&](int64_t t) {
+    const T* src = lane_in + t * BT;
+    const int rem = batch_rem(t);
+    if (rem == BATCH) {  // warp-uniform: full batch, unpredicated loads
+#pragma unroll
+      for (int c = 0; c < IN; ++c) {
+        const T* sc = src + c * ld_in;
+#pragma unroll
+        for (int j = 0; j < PW; ++j) load_vec<T, IN == 4>(sc + j * SUB, cur[j][c]);
+      }
+    } else {  // ragged tail: vectors past the end are not loaded (their segments are masked off)
+#pragma unroll
+      for (int j = 0; j < PW; ++j)
+        if (j * SUB + lane * V < rem) {
+#pragma unroll
+          for (int c = 0; c < IN; ++c) load_vec<T, IN == 4>(src + c * ld_in + j * SUB, cur[j][c]);
+        }
+    }
+  };
+  // copy the visible rows of iteration kk (tile tk, buffer cb) to their global rows
+  unsigned cpar = 0;  // bit q: parity of the next phase of mb_pre[q] this warp waits for
+  auto copy_out = [&](int64_t tk, int cb) {
+    mbar_wait_a(mbp_a + 8 * cb, (cpar >> cb) & 1u);
+    cpar ^= 1u << cb;
+    if (warp == 0 && lane == 0) CLIP_TRACE(tk, 6, trace_now());
+    const int cnt = s_cnt[cb][warp];
+    const int64_t g0 = s_prefix[cb] + s_pre[cb][warp];
+    const uint32_t reg = region_of(cb) + lane * ROWB;
+    T* dst[OUT];  // per-plane row pointers, computed once per batch
+#pragma unroll
+    for (int c = 0; c < OUT; ++c) dst[c] = out + c * ld_out + g0 + lane;
+    const uint32_t slix = sbase + (uint32_t)(S::kLixOff + ((size_t)cb * W + warp) * BATCH) + lane;
+    const int64_t ib = INDEX ? index_base + tk * BT + (int64_t)warp * BATCH : 0;
+#pragma unroll
+    for (int q = 0; q < BATCH / 32; ++q) {
+      if (q * 32 >= cnt) break;
+      if (q * 32 + lane < cnt) {
+        T row[IN];
+        lds_row<T, IN>(reg + q * 32 * ROWB, row);
+#pragma unroll
+        for (int c = 0; c < OUT; ++c) __stcs(dst[c] + q * 32, row[c]);
+        if (INDEX) out_index[g0 + q * 32 + lane] = ib + lds_u8(slix + q * 32);
+      }
+    }
+  };
+  // Claims: warp 0's lane 0 issues the fetch-and-add for iteration k + 3 during iteration k
+  // and publishes its result (s_tile, mb_tile) at the start of iteration k + 1, so the atomic's
+  // round trip overlaps a whole iteration of work instead of stalling the claiming warp.
+  const bool claimer = warp == 0 && lane == 0;
+  unsigned long long claimed = claimer ? atom_add_global(counter, 1ull) : 0ull;  // iteration 2
+#pragma unroll
+  for (int j = 0; j < PW; ++j)
+#pragma unroll
+    for (int c = 0; c < IN; ++c)
+#pragma unroll
+      for (int v = 0; v < V; ++v) cur[j][c][v] = T(0);
+  mbar_wait_a(mbt_a, 0u);
+  int64_t tile = s_tile[0];
+  if (tile < ntiles) load(tile);
+  int b = 0;                      // staging buffer of iteration k
+  int64_t pend[NBUF - 1];         // tiles of iterations k-1, k-2, ... still staged
+#pragma unroll
+  for (int q = 0; q < NBUF - 1; ++q) pend[q] = ntiles;
+  int64_t k = 0;
+  for (; tile < ntiles; ++k) {
+    if (claimer) {
+      const int q = (int)((k + 2) & kRingMask);
+      s_tile[q] = (int64_t)claimed;  // claimed during iteration k - 1 (before the loop for k = 0)
+      CLIP_TRACE((int64_t)claimed, 0, trace_now());
+      mbar_arrive_a(mbt_a + 8 * q);
+      claimed = atom_add_global(counter, 1ull);  // iteration k + 3, published next iteration
+    }
+    const uint32_t region = region_of(b);
+    const int rem = batch_rem(tile);
+    if (warp == 0 && lane == 0) CLIP_TRACE(tile, 1, trace_now());
+    // ---- phase 1: R3, and the kept rows listed in segment order
+    unsigned keep[PW];
+    unsigned cnt = 0;  // kept per sub-tile, byte j
+#pragma unroll
+    for (int j = 0; j < PW; ++j) {
+      const int o = j * SUB + lane * V;
+      keep[j] = Op::template keep<V>(cur[j], w, kparams);
+      if (rem < BATCH) keep[j] &= (o >= rem) ? 0u : (o + V <= rem ? (1u << V) - 1u : (1u << (rem - o)) - 1u);
+      cnt |= (unsigned)__popc(keep[j]) << (8 * j);
+    }
+    unsigned incl = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+      if (lane >= d) incl += y;
+    }
+    const unsigned tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    const unsigned excl = incl - cnt;
+    __syncwarp();  // the previous use of this region (a copy-out) is done
+    int before = 0;
+#pragma unroll
+    for (int j = 0; j < PW; ++j) {
+      int pos = before + (int)((excl >> (8 * j)) & 0xFFu);
+#pragma unroll
+      for (int v = 0; v < V; ++v) {
+        const unsigned kv = (keep[j] >> v) & 1u;
+        if (kv) {
+          T row[IN];
+#pragma unroll
+          for (int c = 0; c < IN; ++c) row[c] = cur[j][c][v];
+          sts_row<T, IN>(region + pos * ROWB, row);
+          sts_u8(lidx_a + pos, (uint32_t)(j * SUB + lane * V + v));
+        }
+        pos += kv;
+      }
+      before += (int)((tot >> (8 * j)) & 0xFFu);
+      if (FLAGS) {
+        if constexpr (V == 4) sts_u32(lflag_a + j * SUB + lane * V, 0u);
+        else sts_u16(lflag_a + j * SUB + lane * V, 0u);
+      }
+    }
+    const int nkept = before;
+    __syncwarp();
+    // the next tile's batch, in flight during phase 2
+    mbar_wait_a(mbt_a + 8 * (int)((k + 1) & kRingMask), (uint32_t)(((k + 1) / kTileRing) & 1));
+    const int64_t next = s_tile[(k + 1) & kRingMask];
+    if (next < ntiles) load(next);
+    // ---- phase 2: clip the kept rows (two per lane while more than 32 remain); each
+    // visible row is written back at its rank, which is at most its list position, so rows
+    // still to be read are never overwritten
+    int rank = 0;
+    const uint32_t slix = INDEX ? sbase + (uint32_t)(S::kLixOff + ((size_t)b * W + warp) * BATCH) : 0u;
+    int p0 = 0;
+#if CLIPSEG_PK_ILP >= 2
+    for (; nkept - p0 > 32; p0 += 64) {
+      const int pa = p0 + lane, pb = p0 + 32 + lane;
+      const bool actb = pb < nkept;
+      const int pbr = actb ? pb : pa;  // an idle second item re-clips the first (same path, no divergence)
+      T ra[IN], rb[IN];
+      lds_row<T, IN>(region + pa * ROWB, ra);
+      lds_row<T, IN>(region + pbr * ROWB, rb);
+      const uint32_t ida = lds_u8(lidx_a + pa), idb = lds_u8(lidx_a + pbr);
+      T qa[OUT], qb[OUT];
+      bool va, vb;
+      Op::clip_two(ra, rb, w, qa, qb, va, vb);
+      vb = vb & actb;
+      __syncwarp();
+      const unsigned ma = __ballot_sync(0xFFFFFFFFu, va), mb = __ballot_sync(0xFFFFFFFFu, vb);
+      const int rank_b = rank + __popc(ma);
+      if (va) {
+        const int r = rank + __popc(ma & lt_mask);
+        sts_row<T, OUT>(region + r * ROWB, qa);
+        if (INDEX) sts_u8(slix + r, ida);
+      }
+      if (vb) {
+        const int r = rank_b + __popc(mb & lt_mask);
+        sts_row<T, OUT>(region + r * ROWB, qb);
+        if (INDEX) sts_u8(slix + r, idb);
+      }
+      if (FLAGS) {
+        sts_u8(lflag_a + ida, va ? 1u : 0u);
+        if (actb) sts_u8(lflag_a + idb, vb ? 1u : 0u);
+      }
+      rank = rank_b + __popc(mb);
+    }
+#endif
+    for (; p0 < nkept; p0 += 32) {
+      const int p = p0 + lane;
+      const bool act = p < nkept;
+      const int pr = act ? p : p0;  // an idle lane re-clips the round's first row
+      T row[IN];
+      lds_row<T, IN>(region + pr * ROWB, row);
+      const uint32_t id = lds_u8(lidx_a + pr);
+      T res[OUT];
+      const bool vis = Op::clip_one(row, w, res) & act;
+      __syncwarp();
+      const unsigned m = __ballot_sync(0xFFFFFFFFu, vis);
+      if (vis) {
+        const int r = rank + __popc(m & lt_mask);
+        sts_row<T, OUT>(region + r * ROWB, res);
+        if (INDEX) sts_u8(slix + r, id);
+      }
+      if (FLAGS && act) sts_u8(lflag_a + id, vis ? 1u : 0u);
+      rank += __popc(m);
+    }
+    if (lane == 0) s_cnt[b][warp] = rank;
+    __syncwarp();
+    if (FLAGS) {
+      uint8_t* fl = flags + tile * BT + (int64_t)warp * BATCH;
+      if (rem == BATCH) {
+#pragma unroll
+        for (int j = 0; j < PW; ++j) {
+          const int o = j * SUB + lane * V;
+          if constexpr (V == 4) *reinterpret_cast<uint32_t*>(fl + o) = lds_u32(lflag_a + o);
+          else *reinterpret_cast<uint16_t*>(fl + o) = (uint16_t)(lds_u32(lflag_a + (o & ~3)) >> (8 * (o & 3)));
+        }
+      } else {
+        for (int o = lane; o < rem; o += 32) fl[o] = (uint8_t)lds_u8(lflag_a + o);
+      }
+    }
+    // the last compute warp to finish publishes the tile aggregate (flag A)
+    int last = 0;
+    if (lane == 0) {
+      __threadfence_block();
+      last = atom_add_shared(&s_done[b], 1) == W - 1;
+    }
+    last = __shfl_sync(0xFFFFFFFFu, last, 0);
+    if (last) {
+      __threadfence_block();
+      int c = (lane < W) ? ((volatile int*)s_cnt[b])[lane] : 0;
+      if (W > 32 && lane + 32 < W) c += ((volatile int*)s_cnt[b])[lane + 32];
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xFFFFFFFFu, c, d);
+      if (lane == 0) {
+        st_relaxed(status + tile, kFlagA | (unsigned long long)c);
+        CLIP_TRACE(tile, 2, trace_now());
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive_a(mbc_a + 8 * b);
+    // copy out iteration k - (NBUF-1), NBUF-1 tiles behind: its offsets are known by now
+    b = (b + 1 == NBUF) ? 0 : b + 1;  // buffer of iteration k + 1 == buffer of iteration k - (NBUF-1)
+    if (pend[NBUF - 2] < ntiles) copy_out(pend[NBUF - 2], b);
+#pragma unroll
+    for (int q = NBUF - 2; q > 0; --q) pend[q] = pend[q - 1];
+    pend[0] = tile;
+    tile = next;
+  }
+  // drain: the last NBUF-1 iterations are still staged (oldest first)
+#pragma unroll
+  for (int q = NBUF - 2; q >= 0; --q) {
+    b = (b + 1 == NBUF) ? 0 : b + 1;
+    if (pend[q] < ntiles) copy_out(pend[q], b);
+  }
+}
+
+template <typename T, class Op, bool FLAGS, bool INDEX>
+static cudaError_t launch_packed_variant(const T* in, int64_t ld_in, int64_t n, const typename Op::Params& w, T* out,
                                          int64_t ld_out, int64_t* out_index, int64_t index_base, uint8_t* flags,
                                          int64_t* d_count, unsigned long long* ws, int64_t ntiles, cudaStream_t s) {
-  typedef CompactShape<T, Op, INDEX> S;
-  const size_t smem = S::kSmemBytes;
-  auto kern = clip_compact_kernel<T, Op, FLAGS, INDEX>;
-  static int blocks_per_sm = 0;  // cached device attribute
-  if (!blocks_per_sm) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, S::kThreads, smem);
-    if (e != cudaSuccess || blocks_per_sm < 1) blocks_per_sm = 1;
-  }
-  // block 0 is the global scanner; the cooperative launch keeps every block resident, so
-  // the scanner runs alongside the tiles it waits on
+  typedef PackedShape<T, Op, INDEX> S;
+  auto kern = clip_compact_packed_kernel<T, Op, FLAGS, INDEX>;
+  int blocks_per_sm = 0;
+  cudaError_t e = kernel_occupancy((const void*)kern, S::kThreads, S::kSmemBytes, &blocks_per_sm);
+  if (e != cudaSuccess) return e;
   const int64_t cap = (int64_t)device_sm_count() * blocks_per_sm;
   const int grid = (int)(ntiles + 1 < cap ? ntiles + 1 : cap);
   void* args[] = {(void*)&in,     (void*)&ld_in,     (void*)&n,          (void*)&w,     (void*)&out,
                   (void*)&ld_out, (void*)&out_index, (void*)&index_base, (void*)&flags, (void*)&d_count,
                   (void*)&ws,     (void*)&ntiles};
-  return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(S::kThreads), args, smem, s);
+  return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(S::kThreads), args, S::kSmemBytes, s);
 }
 
+template <typename T, class Op, bool FLAGS, bool INDEX>
+static cudaError_t launch_compact_variant(const T* in, int64_t ld_in, int64_t n, const typename Op::Params& w, T* out,
+                                         int64_t ld_out, int64_t* out_index, int64_t index_base, uint8_t* flags,
+                                         int64_t* d_count, unsigned long long* ws, int64_t ntiles, cudaStream_t s) {
+  if constexpr (compact_packed<T, Op>()) {
+    return launch_packed_variant<T, Op, FLAGS, INDEX>(in, ld_in, n, w, out, ld_out, out_index, index_base, flags,
+                                                      d_count, ws, ntiles, s);
+  } else {
+    typedef CompactShape<T, Op, INDEX> S;
+    const size_t smem = S::kSmemBytes;
+    auto kern = clip_compact_kernel<T, Op, FLAGS, INDEX>;
+    int blocks_per_sm = 0;
+    cudaError_t e = kernel_occupancy((const void*)kern, S::kThreads, smem, &blocks_per_sm);
+    if (e != cudaSuccess) return e;
+    // block 0 is the global scanner; the cooperative launch keeps every block resident, so
+    // the scanner runs alongside the tiles it waits on
+    const int64_t cap = (int64_t)device_sm_count() * blocks_per_sm;
+    const int grid = (int)(ntiles + 1 < cap ? ntiles + 1 : cap);
+    void* args[] = {(void*)&in,     (void*)&ld_in,     (void*)&n,          (void*)&w,     (void*)&out,
+                    (void*)&ld_out, (void*)&out_index, (void*)&index_base, (void*)&flags, (void*)&d_count,
+                    (void*)&ws,     (void*)&ntiles};
+    return cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(S::kThreads), args, smem, s);
+  }
+}
+
+// Block tile of the instantiation launch_compact uses for (T, Op).
+template <typename T, class Op> constexpr int64_t compact_tile() {
+  if constexpr (compact_packed<T, Op>()) return PackedShape<T, Op, false>::BT;
+  else return CompactShape<T, Op, false>::BT;  // the tile size does not depend on out_index
+}
+
+// One launch per call: the workspace (header + one status word per tile) is all zero on
+// entry — zero-filled once by the caller before its first use — and the kernel leaves it
+// all zero again (tile_scan_warp, block_exit), so no per-call memset is needed.
 template <typename T, class Op>
 cudaError_t launch_compact(const T* in, int64_t ld_in, int64_t n, const typename Op::Params& w, T* out,
                            int64_t ld_out, int64_t* out_index, int64_t index_base, uint8_t* flags, int64_t* d_count,
                            void* ws, cudaStream_t s) {
-  typedef CompactShape<T, Op, false> S;  // the tile size does not depend on out_index
-  const int64_t ntiles = (n + S::BT - 1) / S::BT;
-  cudaError_t e = cudaMemsetAsync(ws, 0, kWsHeaderBytes + (size_t)ntiles * 8, s);
-  if (e != cudaSuccess) return e;
+  const int64_t ntiles = (n + compact_tile<T, Op>() - 1) / compact_tile<T, Op>();
   unsigned long long* wsp = reinterpret_cast<unsigned long long*>(ws);
   // flags / out_index are optional outputs: one instantiation per combination, so the
   // per-segment code carries no test for them

@@ -19,6 +19,26 @@ template <typename T, int D> struct BoxOp {  // axis-aligned closed box, D = 2, 
   static __device__ __forceinline__ unsigned group(const T (&pl)[IN][V], const Params& w, T (&res)[OUT][V]) {
     return clip_group<T, D, V, NAN_FILL>(pl, w, res);
   }
+  // packed compacting kernel: R3 alone (bit v: segment v is not rejected) and the clip of
+  // one segment R3 kept
+  // R3 alone (bit v set: segment v kept); KeepParams are prepared once per launch
+#ifndef CLIPSEG_PK_KEEP
+#define CLIPSEG_PK_KEEP 0  // fp32 R3 test: 0 min/max compares (measured faster), 1 sign bits (FMA pipe + LOP3)
+#endif
+  typedef KeepPrep<T, D> KeepParams;
+  static __device__ __forceinline__ KeepParams keep_params(const Params& w) { return keep_prep<T, D>(w); }
+  template <int V>
+  static __device__ __forceinline__ unsigned keep(const T (&pl)[IN][V], const Params& w, const KeepParams& kp) {
+    if constexpr (sizeof(T) == 4 && CLIPSEG_PK_KEEP == 1) return box_keep_sign<D, V>(pl, kp);
+    else return box_keep<T, D, V>(pl, w);
+  }
+  static __device__ __forceinline__ bool clip_one(const T (&P)[IN], const Params& w, T (&Q)[OUT]) {
+    return clip_kept<T, D, false>(P, w, Q);
+  }
+  static __device__ __forceinline__ void clip_two(const T (&Pa)[IN], const T (&Pb)[IN], const Params& w,
+                                                  T (&Qa)[OUT], T (&Qb)[OUT], bool& va, bool& vb) {
+    clip_kept2<T, D, false>(Pa, Pb, w, Qa, Qb, va, vb);
+  }
 };
 struct NoParams {
   int unused;
@@ -198,10 +218,37 @@ template <typename T, class Op> __host__ __device__ constexpr bool compact_prefe
          : Op::IN == 4 && sizeof(T) == 4 ? CLIPSEG_F32_2D_PREFETCH != 0
                                          : true;
 }
+// Packed compacting kernel (clip_compact.cu): warp batches of PW sub-tiles; R3-rejected
+// segments are dropped before the clip and the kept ones are clipped 32 at a time, one
+// per lane.  Knobs: compute warps, sub-tiles per warp batch, staged tiles.
+#ifndef CLIPSEG_PACKED_F32_2D
+#define CLIPSEG_PACKED_F32_2D 1
+#endif
+#ifndef CLIPSEG_PK_WARPS
+#define CLIPSEG_PK_WARPS 15
+#endif
+#ifndef CLIPSEG_PK_PW
+#define CLIPSEG_PK_PW 2
+#endif
+#ifndef CLIPSEG_PK_ILP
+#define CLIPSEG_PK_ILP 2  // kept rows clipped per lane per round while more than 32 remain
+#endif
+#ifndef CLIPSEG_PK_NBUF
+#define CLIPSEG_PK_NBUF 3
+#endif
+template <typename T, class Op> __host__ __device__ constexpr bool compact_packed() {
+  return compact_headline<T, Op>() && CLIPSEG_PACKED_F32_2D != 0;
+}
+struct PackedKnobs {
+  int warps, pw, nbuf;
+};
+template <typename T, class Op> __host__ __device__ constexpr PackedKnobs packed_knobs() {
+  return PackedKnobs{CLIPSEG_PK_WARPS, CLIPSEG_PK_PW, CLIPSEG_PK_NBUF};
+}
 template <typename T, class Op> __host__ __device__ constexpr int compact_min_blocks() {
   return compact_headline<T, Op>() ? CLIPSEG_MINB_F32_2D : 1;
 }
-// Smallest block tile over all (T, D): the workspace is sized with it.
+// Smallest block tile over all (T, D) and both compacting kernels: the workspace is sized with it.
 constexpr int64_t kMinCompactTile = 8 * 128;
 
 template <typename T, class Op>
@@ -245,5 +292,10 @@ cudaError_t launch_clip_int(const int32_t* in, int64_t ld_in, int64_t n, const i
 
 // Number of SMs of the current device (cached per device).
 int device_sm_count();
+// Resident blocks per SM of `kern` with `threads` threads and `smem` dynamic shared bytes on
+// the current device, after raising the kernel's dynamic shared-memory limit on that device
+// when smem > 48 KB.  Cached per (kernel, device); thread-safe.  Fails (no launch possible)
+// rather than guessing when the kernel cannot be resident.
+cudaError_t kernel_occupancy(const void* kern, int threads, size_t smem, int* blocks_per_sm);
 
 }  // namespace clipseg

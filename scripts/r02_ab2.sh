@@ -1,0 +1,3 @@
+timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_canary.py tests/test_gpu_fullsize.py -m gpu -q -x > gpurun_out/r02d_tests.txt 2>&1; tail -3 gpurun_out/r02d_tests.txt
+bash scripts/ab_compact.sh 1000000000 3 old pk pk15 pk14 > gpurun_out/r02d_ab.txt 2>&1; cat gpurun_out/r02d_ab.txt
+bash scripts/prof_variant.sh pk r02d

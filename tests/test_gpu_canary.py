@@ -73,6 +73,7 @@ def compact_bufs(torch, cs, n, rows, dtype):
     b.g_cnt = Guarded(torch, 0, 1, torch.int64)
     b.g_ws = Guarded(torch, 0, max(int(cs.clip_compact_workspace_bytes(n)), 1), torch.uint8)
     b.out, b.index, b.flags, b.count, b.ws = b.g_out.t, b.g_idx.t, b.g_fl.t, b.g_cnt.t, b.g_ws.t
+    b.ws.zero_()  # the workspace contract: zero-filled before first use
     return b
 
 
@@ -82,6 +83,7 @@ def check_compact_guards(b, n, cnt):
     assert b.g_fl.untouched_from(n), "flags past n written"
     assert b.g_cnt.untouched_from(1)
     assert b.g_ws.untouched_from(b.ws.numel()), "workspace overrun"
+    assert not b.ws.any().item(), "workspace not left zero-filled for the next call"
 
 
 @pytest.mark.parametrize("dim,dt,n", [(2, np.float32, 70001), (2, np.float64, 20011), (3, np.float32, 30011),
