@@ -672,13 +672,21 @@ template <typename T, class Op, bool INDEX> struct PackedShape {
   static constexpr int BATCH = PW * SUB; // segments per warp batch (local indices are bytes)
   static constexpr int W = K.warps;      // compute warps
   static constexpr int BT = W * BATCH;   // segments per block tile
-  static constexpr int NBUF = K.nbuf;    // staged tiles (the copy-out lags NBUF-1 tiles)
   static constexpr size_t ROWB = (size_t)IN * sizeof(T);
   static constexpr size_t kRegion = (size_t)BATCH * IN;               // elements per warp region
+  // staged tiles (the copy-out lags NBUF-1 tiles): the knob, or fewer when they do not fit
+  static constexpr size_t kPerBuf = (size_t)W * (kRegion * sizeof(T) + (INDEX ? BATCH : 0));
+  static constexpr size_t kFixed = (size_t)W * (BATCH / 32 + 1) * 4 + ((size_t)4 << (2 * V)) + (INDEX ? (size_t)W * BATCH : 0);
+  static constexpr int NBUF = (size_t)K.nbuf * kPerBuf + kFixed <= kMaxSmemPerBlock
+                                  ? K.nbuf
+                                  : (int)((kMaxSmemPerBlock - kFixed) / kPerBuf);
   static constexpr size_t kStageBytes = (size_t)NBUF * W * kRegion * sizeof(T);
-  static constexpr size_t kIdxOff = kStageBytes;                      // [W][BATCH] list -> local index
-  static constexpr size_t kFlagOff = kIdxOff + (size_t)W * BATCH;     // [W][BATCH] flag bytes
-  static constexpr size_t kLixOff = kFlagOff + (size_t)W * BATCH;     // [NBUF][W][BATCH] staged indices
+  // per warp: the visible bits of the batch's list, one word per 32 positions (+1 spare word)
+  static constexpr int VBW = BATCH / 32 + 1;
+  static constexpr size_t kVbOff = kStageBytes;                       // [W][VBW] u32
+  static constexpr size_t kLutOff = kVbOff + (size_t)W * VBW * 4;     // [2^(2V)] u32: flags of (keep, bits)
+  static constexpr size_t kIdxOff = kLutOff + ((size_t)4 << (2 * V)); // [W][BATCH] list -> local index (INDEX)
+  static constexpr size_t kLixOff = kIdxOff + (INDEX ? (size_t)W * BATCH : 0);  // [NBUF][W][BATCH] staged indices
   static constexpr size_t kSmemBytes = kLixOff + (INDEX ? (size_t)NBUF * W * BATCH : 0);
   static constexpr int kThreads = (W + 1) * 32;
   static_assert(BATCH <= 256, "local indices are bytes");
@@ -777,6 +785,18 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
   unsigned long long* status = ws + kWsHeaderBytes / 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
+  {  // flags of V segments from their kept mask (high V bits) and the kept ones' visible bits
+    uint32_t* lut = reinterpret_cast<uint32_t*>(smem_raw + S::kLutOff);
+    for (int e = threadIdx.x; e < (1 << (2 * V)); e += blockDim.x) {
+      uint32_t kmask = (uint32_t)e >> V, bits = (uint32_t)e, f = 0;
+      for (int v = 0; v < V; ++v)
+        if ((kmask >> v) & 1u) {
+          f |= (bits & 1u) << (8 * v);
+          bits >>= 1;
+        }
+      lut[e] = f;
+    }
+  }
   if (threadIdx.x == 0) {
     for (int q = 0; q < NBUF; ++q) {
       s_done[q] = 0;
@@ -808,8 +828,9 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
   // ------------------------------------------------------------------ compute warps
   const typename Op::KeepParams kparams = Op::keep_params(w);
   const uint32_t sbase = smem_addr(smem_raw);
-  const uint32_t lidx_a = sbase + (uint32_t)S::kIdxOff + warp * BATCH;    // list position -> local index
-  const uint32_t lflag_a = sbase + (uint32_t)S::kFlagOff + warp * BATCH;  // local index -> flag
+  const uint32_t lidx_a = sbase + (uint32_t)S::kIdxOff + warp * BATCH;    // list position -> local index (INDEX)
+  const uint32_t vb_a = sbase + (uint32_t)S::kVbOff + warp * S::VBW * 4;  // visible bits of the list
+  const uint32_t lut_a = sbase + (uint32_t)S::kLutOff;
   const uint32_t mbt_a = smem_addr(mb_tile), mbc_a = smem_addr(mb_cnt), mbp_a = smem_addr(mb_pre);
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t full_tiles = n / BT;  // tiles whose every batch is full
@@ -857,15 +878,25 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
     for (int c = 0; c < OUT; ++c) dst[c] = out + c * ld_out + g0 + lane;
     const uint32_t slix = sbase + (uint32_t)(S::kLixOff + ((size_t)cb * W + warp) * BATCH) + lane;
     const int64_t ib = INDEX ? index_base + tk * BT + (int64_t)warp * BATCH : 0;
+#ifndef CLIPSEG_PK_COPY_CHUNK
+#define CLIPSEG_PK_COPY_CHUNK 1  // copy-out rounds whose shared loads are issued before their stores
+#endif
+    constexpr int CH = CLIPSEG_PK_COPY_CHUNK;
 #pragma unroll
-    for (int q = 0; q < BATCH / 32; ++q) {
-      if (q * 32 >= cnt) break;
-      if (q * 32 + lane < cnt) {
-        T row[IN];
-        lds_row<T, IN>(reg + q * 32 * ROWB, row);
+    for (int q0 = 0; q0 < BATCH / 32; q0 += CH) {
+      if (q0 * 32 >= cnt) break;
+      T rows[CH][IN];
 #pragma unroll
-        for (int c = 0; c < OUT; ++c) __stcs(dst[c] + q * 32, row[c]);
-        if (INDEX) out_index[g0 + q * 32 + lane] = ib + lds_u8(slix + q * 32);
+      for (int u = 0; u < CH; ++u)
+        if ((q0 + u) * 32 + lane < cnt) lds_row<T, IN>(reg + (q0 + u) * 32 * ROWB, rows[u]);
+#pragma unroll
+      for (int u = 0; u < CH; ++u) {
+        const int q = q0 + u;
+        if (q * 32 + lane < cnt) {
+#pragma unroll
+          for (int c = 0; c < OUT; ++c) __stcs(dst[c] + q * 32, rows[u][c]);
+          if (INDEX) out_index[g0 + q * 32 + lane] = ib + lds_u8(slix + q * 32);
+        }
       }
     }
   };
@@ -919,9 +950,11 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
     const unsigned excl = incl - cnt;
     __syncwarp();  // the previous use of this region (a copy-out) is done
     int before = 0;
+    int kbase[PW];  // list position of this lane's first kept segment of sub-tile j
 #pragma unroll
     for (int j = 0; j < PW; ++j) {
       int pos = before + (int)((excl >> (8 * j)) & 0xFFu);
+      kbase[j] = pos;
 #pragma unroll
       for (int v = 0; v < V; ++v) {
         const unsigned kv = (keep[j] >> v) & 1u;
@@ -930,15 +963,11 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
 #pragma unroll
           for (int c = 0; c < IN; ++c) row[c] = cur[j][c][v];
           sts_row<T, IN>(region + pos * ROWB, row);
-          sts_u8(lidx_a + pos, (uint32_t)(j * SUB + lane * V + v));
+          if (INDEX) sts_u8(lidx_a + pos, (uint32_t)(j * SUB + lane * V + v));
         }
         pos += kv;
       }
       before += (int)((tot >> (8 * j)) & 0xFFu);
-      if (FLAGS) {
-        if constexpr (V == 4) sts_u32(lflag_a + j * SUB + lane * V, 0u);
-        else sts_u16(lflag_a + j * SUB + lane * V, 0u);
-      }
     }
     const int nkept = before;
     __syncwarp();
@@ -960,10 +989,15 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       T ra[IN], rb[IN];
       lds_row<T, IN>(region + pa * ROWB, ra);
       lds_row<T, IN>(region + pbr * ROWB, rb);
-      const uint32_t ida = lds_u8(lidx_a + pa), idb = lds_u8(lidx_a + pbr);
+      const uint32_t ida = INDEX ? lds_u8(lidx_a + pa) : 0u, idb = INDEX ? lds_u8(lidx_a + pbr) : 0u;
       T qa[OUT], qb[OUT];
       bool va, vb;
+#ifdef CLIPSEG_ABL_NOMATH  // ablation builds only: the framework without the clip
+      for (int c = 0; c < OUT; ++c) { qa[c] = ra[c]; qb[c] = rb[c]; }
+      va = ra[0] < ra[2]; vb = rb[0] < rb[2];
+#else
       Op::clip_two(ra, rb, w, qa, qb, va, vb);
+#endif
       vb = vb & actb;
       __syncwarp();
       const unsigned ma = __ballot_sync(0xFFFFFFFFu, va), mb = __ballot_sync(0xFFFFFFFFu, vb);
@@ -978,9 +1012,9 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
         sts_row<T, OUT>(region + r * ROWB, qb);
         if (INDEX) sts_u8(slix + r, idb);
       }
-      if (FLAGS) {
-        sts_u8(lflag_a + ida, va ? 1u : 0u);
-        if (actb) sts_u8(lflag_a + idb, vb ? 1u : 0u);
+      if (FLAGS && lane == 0) {
+        sts_u32(vb_a + 4 * (p0 >> 5), ma);
+        sts_u32(vb_a + 4 * (p0 >> 5) + 4, mb);
       }
       rank = rank_b + __popc(mb);
     }
@@ -991,9 +1025,14 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       const int pr = act ? p : p0;  // an idle lane re-clips the round's first row
       T row[IN];
       lds_row<T, IN>(region + pr * ROWB, row);
-      const uint32_t id = lds_u8(lidx_a + pr);
+      const uint32_t id = INDEX ? lds_u8(lidx_a + pr) : 0u;
       T res[OUT];
+#ifdef CLIPSEG_ABL_NOMATH
+      for (int c = 0; c < OUT; ++c) res[c] = row[c];
+      const bool vis = (row[0] < row[2]) & act;
+#else
       const bool vis = Op::clip_one(row, w, res) & act;
+#endif
       __syncwarp();
       const unsigned m = __ballot_sync(0xFFFFFFFFu, vis);
       if (vis) {
@@ -1001,22 +1040,28 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
         sts_row<T, OUT>(region + r * ROWB, res);
         if (INDEX) sts_u8(slix + r, id);
       }
-      if (FLAGS && act) sts_u8(lflag_a + id, vis ? 1u : 0u);
+      if (FLAGS && lane == 0) sts_u32(vb_a + 4 * (p0 >> 5), m);
       rank += __popc(m);
     }
     if (lane == 0) s_cnt[b][warp] = rank;
     __syncwarp();
     if (FLAGS) {
+      // this lane's kept segments of sub-tile j sit at list positions kbase[j], kbase[j] + 1, ...:
+      // their visible bits are a run of the bitmap, spread back to the kept slots by the table
       uint8_t* fl = flags + tile * BT + (int64_t)warp * BATCH;
-      if (rem == BATCH) {
 #pragma unroll
-        for (int j = 0; j < PW; ++j) {
-          const int o = j * SUB + lane * V;
-          if constexpr (V == 4) *reinterpret_cast<uint32_t*>(fl + o) = lds_u32(lflag_a + o);
-          else *reinterpret_cast<uint16_t*>(fl + o) = (uint16_t)(lds_u32(lflag_a + (o & ~3)) >> (8 * (o & 3)));
+      for (int j = 0; j < PW; ++j) {
+        const int o = j * SUB + lane * V;
+        const uint32_t wa = vb_a + 4 * (kbase[j] >> 5);
+        const uint32_t run = __funnelshift_r(lds_u32(wa), lds_u32(wa + 4), kbase[j] & 31) & ((1u << V) - 1u);
+        const uint32_t f = lds_u32(lut_a + 4 * ((keep[j] << V) | run));
+        if (rem == BATCH || o + V <= rem) {
+          if constexpr (V == 4) *reinterpret_cast<uint32_t*>(fl + o) = f;
+          else *reinterpret_cast<uint16_t*>(fl + o) = (uint16_t)f;
+        } else {
+          for (int v = 0; v < V; ++v)
+            if (o + v < rem) fl[o + v] = (uint8_t)(f >> (8 * v));
         }
-      } else {
-        for (int o = lane; o < rem; o += 32) fl[o] = (uint8_t)lds_u8(lflag_a + o);
       }
     }
     // the last compute warp to finish publishes the tile aggregate (flag A)
