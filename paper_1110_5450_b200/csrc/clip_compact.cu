@@ -894,7 +894,13 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
         const int q = q0 + u;
         if (q * 32 + lane < cnt) {
 #pragma unroll
-          for (int c = 0; c < OUT; ++c) __stcs(dst[c] + q * 32, rows[u][c]);
+          for (int c = 0; c < OUT; ++c) {
+#if CLIPSEG_STORE_HINT == 1
+            dst[c][q * 32] = rows[u][c];
+#else
+            __stcs(dst[c] + q * 32, rows[u][c]);
+#endif
+          }
           if (INDEX) out_index[g0 + q * 32 + lane] = ib + lds_u8(slix + q * 32);
         }
       }
@@ -975,6 +981,38 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
     mbar_wait_a(mbt_a + 8 * (int)((k + 1) & kRingMask), (uint32_t)(((k + 1) / kTileRing) & 1));
     const int64_t next = s_tile[(k + 1) & kRingMask];
     if (next < ntiles) load(next);
+#ifndef CLIPSEG_PK_ILCOPY
+#define CLIPSEG_PK_ILCOPY 0  // copy-out rounds interleaved with phase 2 when the offsets are already known
+#endif
+    // The pending copy-out (iteration k - (NBUF-1), buffer cb): when its offsets have already
+    // arrived, one 32-row round of it runs in each phase-2 round, overlapping its shared
+    // loads and global stores with the clip arithmetic; otherwise it runs (and waits) after.
+    const int cb = (b + 1 == NBUF) ? 0 : b + 1;
+    bool early = false;
+    int ccnt = 0, cq = 0;
+    uint32_t creg = 0;
+    T* cdst[OUT];
+    if (CLIPSEG_PK_ILCOPY && pend[NBUF - 2] < ntiles && !INDEX &&
+        mbar_test_a(mbp_a + 8 * cb, (cpar >> cb) & 1u)) {
+      early = true;
+      cpar ^= 1u << cb;
+      ccnt = s_cnt[cb][warp];
+      creg = region_of(cb) + lane * ROWB;
+      const int64_t g0 = s_prefix[cb] + s_pre[cb][warp];
+#pragma unroll
+      for (int c = 0; c < OUT; ++c) cdst[c] = out + c * ld_out + g0 + lane;
+    }
+    auto copy_round = [&]() {  // warp-uniform: one 32-row round of the early copy-out
+      if (cq * 32 < ccnt) {
+        if (cq * 32 + lane < ccnt) {
+          T row[IN];
+          lds_row<T, IN>(creg + cq * 32 * ROWB, row);
+#pragma unroll
+          for (int c = 0; c < OUT; ++c) __stcs(cdst[c] + cq * 32, row[c]);
+        }
+        ++cq;
+      }
+    };
     // ---- phase 2: clip the kept rows (two per lane while more than 32 remain); each
     // visible row is written back at its rank, which is at most its list position, so rows
     // still to be read are never overwritten
@@ -1000,6 +1038,10 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
 #endif
       vb = vb & actb;
       __syncwarp();
+      if (early) {
+        copy_round();
+        copy_round();
+      }
       const unsigned ma = __ballot_sync(0xFFFFFFFFu, va), mb = __ballot_sync(0xFFFFFFFFu, vb);
       const int rank_b = rank + __popc(ma);
       if (va) {
@@ -1034,6 +1076,7 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       const bool vis = Op::clip_one(row, w, res) & act;
 #endif
       __syncwarp();
+      if (early) copy_round();
       const unsigned m = __ballot_sync(0xFFFFFFFFu, vis);
       if (vis) {
         const int r = rank + __popc(m & lt_mask);
@@ -1085,8 +1128,12 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
     __syncwarp();
     if (lane == 0) mbar_arrive_a(mbc_a + 8 * b);
     // copy out iteration k - (NBUF-1), NBUF-1 tiles behind: its offsets are known by now
-    b = (b + 1 == NBUF) ? 0 : b + 1;  // buffer of iteration k + 1 == buffer of iteration k - (NBUF-1)
-    if (pend[NBUF - 2] < ntiles) copy_out(pend[NBUF - 2], b);
+    b = cb;  // buffer of iteration k + 1 == buffer of iteration k - (NBUF-1)
+    if (early) {
+      while (cq * 32 < ccnt) copy_round();
+    } else if (pend[NBUF - 2] < ntiles) {
+      copy_out(pend[NBUF - 2], b);
+    }
 #pragma unroll
     for (int q = NBUF - 2; q > 0; --q) pend[q] = pend[q - 1];
     pend[0] = tile;
