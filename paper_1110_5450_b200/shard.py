@@ -32,14 +32,42 @@ class ShardResult:
     counts: object      # allgathered counts (device int64[world])
 
 
+def nccl_exchange(count, world, group=None):
+    """All-gather of the per-rank visible counts (int64[1] device tensors) over NCCL."""
+    import torch  # noqa: PLC0415
+    import torch.distributed as dist  # noqa: PLC0415
+
+    counts = torch.empty(world, dtype=torch.int64, device=count.device)
+    dist.all_gather_into_tensor(counts, count, group=group)
+    return counts
+
+
+def host_exchange(count, world, group=None):
+    """The same exchange through host memory, for process groups whose backend cannot gather
+    device tensors (gloo): count -> host, all_gather, counts -> the count's device."""
+    import torch  # noqa: PLC0415
+    import torch.distributed as dist  # noqa: PLC0415
+
+    parts = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(parts, count.cpu(), group=group)
+    return torch.cat(parts).to(count.device)
+
+
 def sharded_compact(local_planes, n_local, lo, hi, start, group=None, bufs=None, stream=None,
-                    compact_fn=None, offsets_fn=None):
+                    compact_fn=None, offsets_fn=None, exchange_fn=None):
     """Compact this rank's shard and fix its global output offset.
 
     compact_fn(planes, n, lo, hi, bufs, index_base) -> bufs with .count (int64[1] tensor);
-    offsets_fn(counts, rank) -> int64[2] tensor (offset, total).  Defaults: the CUDA path."""
-    import torch.distributed as dist  # noqa: PLC0415
+    offsets_fn(counts, rank) -> int64[2] tensor (offset, total);
+    exchange_fn(count, world, group) -> int64[world] counts (default: nccl_exchange).
+    Defaults: the CUDA path.  Every step is issued on `stream` (torch's current stream when
+    None): the compaction, the allgather (NCCL orders against the current stream, which is
+    `stream` inside the block) and the offsets kernel, so none reads a count before it is
+    written."""
+    import contextlib  # noqa: PLC0415
+
     import torch  # noqa: PLC0415
+    import torch.distributed as dist  # noqa: PLC0415
 
     if compact_fn is None or offsets_fn is None:
         from . import clipseg  # noqa: PLC0415
@@ -49,10 +77,12 @@ def sharded_compact(local_planes, n_local, lo, hi, start, group=None, bufs=None,
 
         compact_fn = compact_fn or _cf
         offsets_fn = offsets_fn or (lambda c, r: clipseg.shard_offsets(c, r, stream=stream))
+    exchange_fn = exchange_fn or nccl_exchange
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    bufs = compact_fn(local_planes, n_local, lo, hi, bufs, start)
-    counts = torch.empty(world, dtype=torch.int64, device=bufs.count.device)
-    dist.all_gather_into_tensor(counts, bufs.count, group=group)
-    offsets = offsets_fn(counts, rank)
+    ctx = torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+    with ctx:
+        bufs = compact_fn(local_planes, n_local, lo, hi, bufs, start)
+        counts = exchange_fn(bufs.count, world, group)
+        offsets = offsets_fn(counts, rank)
     return ShardResult(start=start, count=bufs.count, offsets=offsets, counts=counts), bufs

@@ -285,16 +285,31 @@ def test_idempotence():
     assert np.array_equal(_bits_arr(out2), _bits_arr(again))
 
 
-@pytest.mark.parametrize("k", [-7, 5])
-def test_power_of_two_scaling(k):
-    n = 100000
-    planes, _ = synth.fill_host(synth.UNIFORM, 2, synth.seed_for(1, 5), n)
-    out, flags = oracle.clip(planes, n, *UNIT2, 2)
-    s = np.float32(2.0 ** k)
-    out_s, flags_s = oracle.clip(planes * s, n, [0, 0], [float(s), float(s)], 2)
+@pytest.mark.parametrize("dt", [np.float32, np.float64])
+@pytest.mark.parametrize("dim", [2, 3])
+@pytest.mark.parametrize("k", [-40, -20, -7, 5, 20, 40, 57])
+def test_power_of_two_scaling(k, dim, dt):
+    """Scaling inputs and window by 2^k scales every result by 2^k exactly: each rule is a
+    correctly rounded operation, and RN(2^k x) = 2^k RN(x) while nothing under- or
+    overflows (operands stay within [2^-62, 2^59] for fp32).  The range spans the GPU fast
+    path's whole claimed operand range (tests/test_gpu_wide.py runs the same windows)."""
+    n = 20000
+    planes, _ = synth.fill_host(synth.UNIFORM, dim, synth.seed_for(1, 5), n, dtype=dt)
+    lo, hi = [0.0] * dim, [1.0] * dim
+    out, flags = oracle.clip(planes, n, lo, hi, dim)
+    s = dt(2.0 ** k)
+    out_s, flags_s = oracle.clip(planes * s, n, lo, [float(s)] * dim, dim)
     assert np.array_equal(flags, flags_s)
     v = flags.astype(bool)
+    assert v.sum() > 0
     assert np.array_equal(_bits_arr(out_s[:, :n][:, v]), _bits_arr(out[:, :n][:, v] * s))
+    # the symmetric window [-2^k, 2^k]^D against [-1, 1]^D
+    sym = planes * dt(2) - dt(1)
+    out1, fl1 = oracle.clip(sym, n, [-1.0] * dim, [1.0] * dim, dim)
+    out2, fl2 = oracle.clip(sym * s, n, [float(-s)] * dim, [float(s)] * dim, dim)
+    assert np.array_equal(fl1, fl2)
+    v = fl1.astype(bool)
+    assert np.array_equal(_bits_arr(out2[:, :n][:, v]), _bits_arr(out1[:, :n][:, v] * s))
 
 
 def test_mirror_and_transpose():
