@@ -250,12 +250,14 @@ def main():
         if world > 1:
             dist.barrier()
     ms = t0.elapsed_time(t1)
-    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev)
+    kts = [a.elapsed_time(b) for a, b in kev]
+    kern_ms = statistics.mean(kts)
+    kern_med, kern_best = statistics.median(kts), min(kts)
     cnt = int(bufs.count.item())
     if world > 1:
-        t = torch.tensor([ms, kern_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms, kern_ms, kern_med, kern_best], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, kern_ms = float(t[0]), float(t[1])
+        ms, kern_ms, kern_med, kern_best = float(t[0]), float(t[1]), float(t[2]), float(t[3])
         total = torch.tensor([cnt], dtype=torch.int64, device=dev)
         dist.all_reduce(total)
         visible_total = int(total.item())
@@ -293,6 +295,14 @@ def main():
     configs = None
     if rank == 0 and world == 1 and not args.no_configs:
         configs = run_config_sweep(torch, clipseg, synth, dev, stream)
+    # secondary C5 mix row at full size (same buffers, regenerated) and the per-step fixed
+    # cost of the sharded step at the N=8 per-rank size
+    mix_row = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        mix_row = run_c5_mix(torch, clipseg, synth, planes, bufs, n, stream)
+    fixed = None
+    if world == 1 and not args.no_configs:
+        fixed = run_fixed_cost(torch, dist, clipseg, synth, dev, stream)
     next3 = None
     if rank == 0 and world == 1 and not args.no_next3:
         next3 = run_next3(torch, clipseg, dev, stream)
@@ -306,9 +316,14 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         nth = min(host_threads(), 64)
         r, dt, nth, passes = cpu_oracle_rate(args.cpu_sample, nth, 10.0)
+        s1 = max(args.cpu_sample // 16, 1_000_000)
+        r1, dt1, _, passes1 = cpu_oracle_rate(s1, 1, 4.0)
         cpu = {"value": r, "unit": "segments/s", "cores": nth, "kind": "oracle",
                "sample": f"first {args.cpu_sample} segments of the workload, {passes} passes in {dt:.1f} s "
-                         f"wall on {nth} threads (static split)"}
+                         f"wall on {nth} threads (static split)",
+               "value_1_thread": r1,
+               "sample_1_thread": f"first {s1} segments, {passes1} passes in {dt1:.1f} s on 1 thread",
+               "cpu_model": cpu_model(), "nproc": os.cpu_count()}
 
     if world > 1:
         dist.barrier()
@@ -326,7 +341,10 @@ def main():
                    "parallelism": f"shard{world} (contiguous; NCCL allgather of counts)"},
         "hbm_gbs_step": alg_bytes / (ms_per_step / 1e3) / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "clip_compact_kernel<float,2>", "kernel_ms": kern_ms,
+                     "frac_vs_measured": achieved / peak, "frac_vs_8tbs": achieved / 8000.0,
+                     "traffic": traffic, "kernel": "clip_compact_packed_kernel<float,BoxOp<float,2>,1,0>",
+                     "kernel_ms": kern_ms, "kernel_ms_median": kern_med, "kernel_ms_best": kern_best,
+                     "kernel_ms_stat": f"mean (median, best) over {args.steps} steps",
                      "alg_bytes_per_launch": alg_bytes, "peak_source": peak_src},
         "clocks": clk.summary(),
         "gpu_launches": launches_per_step * args.steps,
@@ -334,6 +352,8 @@ def main():
         "cpu_baseline": cpu,
         "parity": parity,
         "configs": configs,
+        "c5_mix_33": mix_row,
+        "fixed_cost": fixed,
         "next1": next1,
         "next2": next2,
         "next4": next4,
@@ -365,6 +385,118 @@ def sampled_parity(torch, bufs, n, start, rank, m=2000):
     ok = ok and np.array_equal(got.view(np.uint32), want[:, vis].view(np.uint32))
     del pos
     return f"{'ok' if ok else 'MISMATCH'}: {len(idx)} sampled segments bit-exact vs oracle"
+
+
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_c5_mix(torch, clipseg, synth, planes, bufs, n, stream, steps=10):
+    """C5's secondary row: the same 1e9-segment compacting clip on the MIX
+    family with a 1/3 inside, 1/3 crossing, 1/3 outside mix, regenerated into the headline's
+    buffers after the headline was timed."""
+    pin, pc = synth.mix_thresholds(1 / 3, 1 / 3)
+    synth.fill_device(planes, synth.MIX, DIM, synth.seed_for(5, 33), n, p_in=pin, p_cross=pc)
+    w = clipseg.make_window([0.0, 0.0], [1.0, 1.0])
+    sp = stream.cuda_stream
+
+    def one():
+        st = clipseg.clip_segments_compact_f32(planes.data_ptr(), planes.stride(0), n, ctypes.byref(w),
+                                               bufs.out.data_ptr(), bufs.out.stride(0), None, 0,
+                                               bufs.flags.data_ptr(), bufs.count.data_ptr(), bufs.ws.data_ptr(),
+                                               bufs.ws.numel(), sp)
+        if st != 0:
+            raise RuntimeError(clipseg.clip_status_string(st))
+
+    for _ in range(3):
+        one()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        one()
+        b.record(stream)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    cnt = int(bufs.count.item())
+    ms = statistics.median(ts)
+    alg = n * (2 * DIM * 4 + 1) + cnt * 2 * DIM * 4
+    peak, _ = measured_peak()
+    return {"workload": "C5 mix: 1e9 2D fp32 segments, MIX family 1/3 inside, 1/3 crossing, 1/3 outside, "
+                        "window [0,1]^2, compacting clip + flags",
+            "value": n / (ms / 1e3), "unit": "segments/s", "ms": ms, "ms_best": min(ts),
+            "visible_fraction": cnt / n, "GBps": alg / ms / 1e6, "frac": alg / ms / 1e6 / peak,
+            "frac_vs_8tbs": alg / ms / 1e6 / 8000.0}
+
+
+def run_fixed_cost(torch, dist, clipseg, synth, dev, stream, n=125_000_000, steps=30):
+    """Per-step fixed cost of the sharded step at the per-rank size of N = 8 (1.25e8): the
+    compacting kernel + the NCCL count allgather + the offsets kernel, on a 1-rank NCCL
+    group; fixed = median(step) - median(kernel), CUDA events on the launching stream."""
+    import socket  # noqa: PLC0415
+    made = False
+    if not dist.is_initialized():
+        with socket.socket() as s_:
+            s_.bind(("127.0.0.1", 0))
+            port = s_.getsockname()[1]
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ["MASTER_PORT"] = str(port)
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=dev)
+        made = True
+    try:
+        planes = clipseg.empty_planes(n, DIM, torch.float32, dev)
+        synth.fill_device(planes, synth.UNIFORM, DIM, SEED, n)
+        bufs = clipseg.CompactBuffers(n, DIM, torch.float32, dev, with_flags=True)
+        counts = torch.zeros(1, dtype=torch.int64, device=dev)
+        offs = torch.zeros(2, dtype=torch.int64, device=dev)
+        w = clipseg.make_window([0.0, 0.0], [1.0, 1.0])
+        sp = stream.cuda_stream
+
+        def step(ev):
+            ev[0].record(stream)
+            st = clipseg.clip_segments_compact_f32(planes.data_ptr(), planes.stride(0), n, ctypes.byref(w),
+                                                   bufs.out.data_ptr(), bufs.out.stride(0), None, 0,
+                                                   bufs.flags.data_ptr(), bufs.count.data_ptr(), bufs.ws.data_ptr(),
+                                                   bufs.ws.numel(), sp)
+            ev[1].record(stream)
+            if st != 0:
+                raise RuntimeError(clipseg.clip_status_string(st))
+            dist.all_gather_into_tensor(counts, bufs.count)
+            clipseg.clip_shard_offsets(counts.data_ptr(), 1, 0, offs.data_ptr(), offs.data_ptr() + 8, sp)
+            ev[2].record(stream)
+
+        mk = lambda: tuple(torch.cuda.Event(enable_timing=True) for _ in range(3))  # noqa: E731
+        for _ in range(3):
+            step(mk())
+        torch.cuda.synchronize()
+        evs = [mk() for _ in range(steps)]
+        for e in evs:
+            step(e)
+        torch.cuda.synchronize()
+        kern = statistics.median(e[0].elapsed_time(e[1]) for e in evs)
+        whole = statistics.median(e[0].elapsed_time(e[2]) for e in evs)
+        del planes, bufs
+        return {"n_per_rank": n, "step_ms": whole, "kernel_ms": kern, "fixed_us": 1e3 * (whole - kern),
+                "budget_us": 60, "what": "median(compact + NCCL allgather of 8 B + offsets kernel) - median(compact),"
+                                         " 1-rank NCCL group, per-rank size of the N=8 run"}
+    finally:
+        if made:
+            dist.destroy_process_group()
 
 
 def run_config_sweep(torch, clipseg, synth, dev, stream, steps=10):
@@ -408,10 +540,26 @@ def run_config_sweep(torch, clipseg, synth, dev, stream, steps=10):
         out = torch.empty_like(planes)
         flags = torch.empty(n, dtype=torch.uint8, device=dev)
         ms_d = timed(lambda: clipseg.clip(planes, n, lo, hi, out=out, flags=flags, stream=stream))
+        near = None
+        if fam == synth.ADVERSARIAL:
+            # the generator's near-boundary segments (tag bit 0x80: an endpoint within tolerance
+            # of an edge), reported separately as north_star asks; for fp32 also the flags that
+            # differ from the same inputs clipped in fp64 (upcast exactly) — fp32-ambiguous cases
+            tag = torch.empty(n, dtype=torch.uint8, device=dev)
+            synth.fill_device(planes, fam, D, synth.seed_for(2), n, p_in=pin, p_cross=pc, tag_t=tag)
+            isnear = (tag & 0x80) != 0
+            near = {"near_tagged": int(isnear.sum())}
+            if dt == torch.float32:
+                _, f64 = clipseg.clip(planes.double(), n, lo, hi, stream=stream)
+                dis = flags[:n] != f64[:n]
+                near["flag_disagree_fp64_near"] = int((dis & isnear).sum())
+                near["flag_disagree_fp64_other"] = int((dis & ~isnear).sum())
+                del f64, dis
+            del tag, isnear
         del out, flags, planes
         bc = n * (2 * D * esz + 1) + cnt * 2 * D * esz
         bd = n * (4 * D * esz + 1)
-        rows.append({"config": name, "visible_fraction": cnt / n,
+        rows.append({"config": name, "visible_fraction": cnt / n, "near_boundary": near,
                      "compact": {"ms": ms_c, "segments_per_s": n / ms_c * 1e3, "GBps": bc / ms_c / 1e6,
                                  "frac": bc / ms_c / 1e6 / peak},
                      "dense": {"ms": ms_d, "segments_per_s": n / ms_d * 1e3, "GBps": bd / ms_d / 1e6,
