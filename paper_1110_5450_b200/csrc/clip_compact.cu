@@ -696,8 +696,8 @@ template <typename T, class Op, bool INDEX> struct PackedShape {
 };
 
 // Shared memory by 32-bit shared-window address (computed once per kernel, so the hot loops
-// carry no generic-to-shared conversions).  Rows of N elements, aligned to 16 B (fp32 rows
-// of 4 or 8, fp64 rows) or 8 B (fp32 rows of 6).
+// carry no generic-to-shared conversions).  Rows of N elements: 128-bit accesses for rows of
+// a multiple of 16 B (fp32 rows of 4 or 8, fp64 rows), 64-bit ones for fp32 rows of 6.
 __device__ __forceinline__ void sts_u8(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u8 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
@@ -719,15 +719,17 @@ __device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
 }
 template <typename T, int N>
 __device__ __forceinline__ void sts_row(uint32_t a, const T (&v)[N]) {
-  if constexpr (sizeof(T) == 4) {
-    static_assert(N % 2 == 0, "row layout");
+  if constexpr (sizeof(T) == 4 && N % 4 == 0) {  // 16-byte rows: 128-bit stores
 #pragma unroll
-    for (int i = 0; i + 4 <= N; i += 4)
+    for (int i = 0; i < N; i += 4)
       asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a + 4 * i), "f"(v[i]), "f"(v[i + 1]),
                    "f"(v[i + 2]), "f"(v[i + 3])
                    : "memory");
-    if constexpr (N % 4 == 2)
-      asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a + 4 * (N - 2)), "f"(v[N - 2]), "f"(v[N - 1]) : "memory");
+  } else if constexpr (sizeof(T) == 4) {  // rows of 6 floats are only 8-byte aligned
+    static_assert(N % 2 == 0, "row layout");
+#pragma unroll
+    for (int i = 0; i < N; i += 2)
+      asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a + 4 * i), "f"(v[i]), "f"(v[i + 1]) : "memory");
   } else {
     static_assert(N % 2 == 0, "row layout");
 #pragma unroll
@@ -737,15 +739,17 @@ __device__ __forceinline__ void sts_row(uint32_t a, const T (&v)[N]) {
 }
 template <typename T, int N>
 __device__ __forceinline__ void lds_row(uint32_t a, T (&v)[N]) {
-  if constexpr (sizeof(T) == 4) {
+  if constexpr (sizeof(T) == 4 && N % 4 == 0) {
 #pragma unroll
-    for (int i = 0; i + 4 <= N; i += 4)
+    for (int i = 0; i < N; i += 4)
       asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                    : "=f"(v[i]), "=f"(v[i + 1]), "=f"(v[i + 2]), "=f"(v[i + 3])
                    : "r"(a + 4 * i)
                    : "memory");
-    if constexpr (N % 4 == 2)
-      asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v[N - 2]), "=f"(v[N - 1]) : "r"(a + 4 * (N - 2)) : "memory");
+  } else if constexpr (sizeof(T) == 4) {
+#pragma unroll
+    for (int i = 0; i < N; i += 2)
+      asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v[i]), "=f"(v[i + 1]) : "r"(a + 4 * i) : "memory");
   } else {
 #pragma unroll
     for (int i = 0; i < N; i += 2)

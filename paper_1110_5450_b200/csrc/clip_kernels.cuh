@@ -236,14 +236,30 @@ template <typename T, class Op> __host__ __device__ constexpr bool compact_prefe
 #ifndef CLIPSEG_PK_NBUF
 #define CLIPSEG_PK_NBUF 3
 #endif
+// fp32 3D cuboid (C4): rows of 24 B, so one sub-tile per warp batch keeps the register
+// prefetch (24 floats) and the staging (15 warps x 3 x 3 KB) within budget.
+#ifndef CLIPSEG_PACKED_F32_3D
+#define CLIPSEG_PACKED_F32_3D 1
+#endif
+#ifndef CLIPSEG_PK3_WARPS
+#define CLIPSEG_PK3_WARPS 15
+#endif
+#ifndef CLIPSEG_PK3_PW
+#define CLIPSEG_PK3_PW 1
+#endif
+#ifndef CLIPSEG_PK3_NBUF
+#define CLIPSEG_PK3_NBUF 3
+#endif
 template <typename T, class Op> __host__ __device__ constexpr bool compact_packed() {
-  return compact_headline<T, Op>() && CLIPSEG_PACKED_F32_2D != 0;
+  return (compact_headline<T, Op>() && CLIPSEG_PACKED_F32_2D != 0) ||
+         (sizeof(T) == 4 && Op::IN == 6 && Op::OUT == 6 && CLIPSEG_PACKED_F32_3D != 0);
 }
 struct PackedKnobs {
   int warps, pw, nbuf;
 };
 template <typename T, class Op> __host__ __device__ constexpr PackedKnobs packed_knobs() {
-  return PackedKnobs{CLIPSEG_PK_WARPS, CLIPSEG_PK_PW, CLIPSEG_PK_NBUF};
+  return Op::IN == 6 ? PackedKnobs{CLIPSEG_PK3_WARPS, CLIPSEG_PK3_PW, CLIPSEG_PK3_NBUF}
+                     : PackedKnobs{CLIPSEG_PK_WARPS, CLIPSEG_PK_PW, CLIPSEG_PK_NBUF};
 }
 template <typename T, class Op> __host__ __device__ constexpr int compact_min_blocks() {
   return compact_headline<T, Op>() ? CLIPSEG_MINB_F32_2D : 1;
