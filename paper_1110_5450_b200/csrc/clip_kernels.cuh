@@ -64,6 +64,22 @@ template <typename T, bool NDC> struct HomogOp {  // NEXT-1: homogeneous clip sp
   static __device__ __forceinline__ unsigned group(const T (&pl)[IN][V], const Params&, T (&res)[OUT][V]) {
     return homog_group<T, V, NAN_FILL, NDC>(pl, res);
   }
+  // packed compacting kernel: H3 alone and the clip of kept segments
+  struct KeepParams {
+    int unused;
+  };
+  static __device__ __forceinline__ KeepParams keep_params(const Params&) { return KeepParams{0}; }
+  template <int V>
+  static __device__ __forceinline__ unsigned keep(const T (&pl)[IN][V], const Params&, const KeepParams&) {
+    return homog_keep<T, V>(pl);
+  }
+  static __device__ __forceinline__ bool clip_one(const T (&P)[IN], const Params&, T (&Q)[OUT]) {
+    return homog_kept<T, NDC>(P, Q);
+  }
+  static __device__ __forceinline__ void clip_two(const T (&Pa)[IN], const T (&Pb)[IN], const Params&, T (&Qa)[OUT],
+                                                  T (&Qb)[OUT], bool& va, bool& vb) {
+    homog_kept2<T, NDC>(Pa, Pb, Qa, Qb, va, vb);
+  }
 };
 
 // Op::group over V segments in chunks of Op::GV (a power of two): bounds the live state of ops
@@ -250,16 +266,28 @@ template <typename T, class Op> __host__ __device__ constexpr bool compact_prefe
 #ifndef CLIPSEG_PK3_NBUF
 #define CLIPSEG_PK3_NBUF 3
 #endif
+// fp32 homogeneous (NEXT-1): rows of 32 B, one sub-tile per warp batch.
+#ifndef CLIPSEG_PACKED_F32_H
+#define CLIPSEG_PACKED_F32_H 1
+#endif
+#ifndef CLIPSEG_PKH_WARPS
+#define CLIPSEG_PKH_WARPS 15
+#endif
+#ifndef CLIPSEG_PKH_NBUF
+#define CLIPSEG_PKH_NBUF 3
+#endif
 template <typename T, class Op> __host__ __device__ constexpr bool compact_packed() {
   return (compact_headline<T, Op>() && CLIPSEG_PACKED_F32_2D != 0) ||
-         (sizeof(T) == 4 && Op::IN == 6 && Op::OUT == 6 && CLIPSEG_PACKED_F32_3D != 0);
+         (sizeof(T) == 4 && Op::IN == 6 && Op::OUT == 6 && CLIPSEG_PACKED_F32_3D != 0) ||
+         (sizeof(T) == 4 && Op::IN == 8 && CLIPSEG_PACKED_F32_H != 0);
 }
 struct PackedKnobs {
   int warps, pw, nbuf;
 };
 template <typename T, class Op> __host__ __device__ constexpr PackedKnobs packed_knobs() {
-  return Op::IN == 6 ? PackedKnobs{CLIPSEG_PK3_WARPS, CLIPSEG_PK3_PW, CLIPSEG_PK3_NBUF}
-                     : PackedKnobs{CLIPSEG_PK_WARPS, CLIPSEG_PK_PW, CLIPSEG_PK_NBUF};
+  return Op::IN == 8   ? PackedKnobs{CLIPSEG_PKH_WARPS, 1, CLIPSEG_PKH_NBUF}
+         : Op::IN == 6 ? PackedKnobs{CLIPSEG_PK3_WARPS, CLIPSEG_PK3_PW, CLIPSEG_PK3_NBUF}
+                       : PackedKnobs{CLIPSEG_PK_WARPS, CLIPSEG_PK_PW, CLIPSEG_PK_NBUF};
 }
 template <typename T, class Op> __host__ __device__ constexpr int compact_min_blocks() {
   return compact_headline<T, Op>() ? CLIPSEG_MINB_F32_2D : 1;
