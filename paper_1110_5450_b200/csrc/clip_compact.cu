@@ -1023,7 +1023,7 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
     int rank = 0;
     const uint32_t slix = INDEX ? sbase + (uint32_t)(S::kLixOff + ((size_t)b * W + warp) * BATCH) : 0u;
     int p0 = 0;
-#if CLIPSEG_PK_ILP >= 2
+    if constexpr (S::K.ilp >= 2) {  // (this instantiation's knob)
     for (; nkept - p0 > 32; p0 += 64) {
       const int pa = p0 + lane, pb = p0 + 32 + lane;
       const bool actb = pb < nkept;
@@ -1064,7 +1064,7 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       }
       rank = rank_b + __popc(mb);
     }
-#endif
+    }
     for (; p0 < nkept; p0 += 32) {
       const int p = p0 + lane;
       const bool act = p < nkept;

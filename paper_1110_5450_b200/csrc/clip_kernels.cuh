@@ -276,18 +276,40 @@ template <typename T, class Op> __host__ __device__ constexpr bool compact_prefe
 #ifndef CLIPSEG_PKH_NBUF
 #define CLIPSEG_PKH_NBUF 3
 #endif
+// fp64 cuboids: 2D rows of 32 B, two sub-tiles of 64 segments per warp batch.
+#ifndef CLIPSEG_PACKED_F64_2D
+#define CLIPSEG_PACKED_F64_2D 1
+#endif
+#ifndef CLIPSEG_PKD_WARPS
+#define CLIPSEG_PKD_WARPS 11
+#endif
+#ifndef CLIPSEG_PKD_PW
+#define CLIPSEG_PKD_PW 2
+#endif
 template <typename T, class Op> __host__ __device__ constexpr bool compact_packed() {
   return (compact_headline<T, Op>() && CLIPSEG_PACKED_F32_2D != 0) ||
          (sizeof(T) == 4 && Op::IN == 6 && Op::OUT == 6 && CLIPSEG_PACKED_F32_3D != 0) ||
-         (sizeof(T) == 4 && Op::IN == 8 && CLIPSEG_PACKED_F32_H != 0);
+         (sizeof(T) == 4 && Op::IN == 8 && CLIPSEG_PACKED_F32_H != 0) ||
+         (sizeof(T) == 8 && Op::IN == 4 && Op::OUT == 4 && CLIPSEG_PACKED_F64_2D != 0);
 }
+// (compute warps, sub-tiles per warp batch, staged tiles, kept rows per lane per round),
+// measured (scripts/ab.sh): two rows per lane pay for 2D fp32 (5.9 -> 5.6 ms at 1e9) and
+// homogeneous fp32 (1.21 -> 1.17 ms at 1e8); one is faster for 3D fp32 (0.92 -> 0.89 ms)
+// and fp64 (adversarial 0.72 -> 0.58 ms at 1e7).
 struct PackedKnobs {
-  int warps, pw, nbuf;
+  int warps, pw, nbuf, ilp;
 };
+#ifndef CLIPSEG_PK3_ILP
+#define CLIPSEG_PK3_ILP 1
+#endif
+#ifndef CLIPSEG_PKD_ILP
+#define CLIPSEG_PKD_ILP 1
+#endif
 template <typename T, class Op> __host__ __device__ constexpr PackedKnobs packed_knobs() {
-  return Op::IN == 8   ? PackedKnobs{CLIPSEG_PKH_WARPS, 1, CLIPSEG_PKH_NBUF}
-         : Op::IN == 6 ? PackedKnobs{CLIPSEG_PK3_WARPS, CLIPSEG_PK3_PW, CLIPSEG_PK3_NBUF}
-                       : PackedKnobs{CLIPSEG_PK_WARPS, CLIPSEG_PK_PW, CLIPSEG_PK_NBUF};
+  return Op::IN == 8          ? PackedKnobs{CLIPSEG_PKH_WARPS, 1, CLIPSEG_PKH_NBUF, CLIPSEG_PK_ILP}
+         : Op::IN == 6        ? PackedKnobs{CLIPSEG_PK3_WARPS, CLIPSEG_PK3_PW, CLIPSEG_PK3_NBUF, CLIPSEG_PK3_ILP}
+         : sizeof(T) == 8     ? PackedKnobs{CLIPSEG_PKD_WARPS, CLIPSEG_PKD_PW, 3, CLIPSEG_PKD_ILP}
+                              : PackedKnobs{CLIPSEG_PK_WARPS, CLIPSEG_PK_PW, CLIPSEG_PK_NBUF, CLIPSEG_PK_ILP};
 }
 template <typename T, class Op> __host__ __device__ constexpr int compact_min_blocks() {
   return compact_headline<T, Op>() ? CLIPSEG_MINB_F32_2D : 1;

@@ -1,3 +1,6 @@
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/r02x_tests.txt 2>&1; tail -2 gpurun_out/r02x_tests.txt
-bash scripts/ab.sh "--kernel compact --n 100000000 --family homog" 2 phoff ph ph11
-bash scripts/ab.sh "--kernel compact --n 100000000 --family homog --ndc 1" 2 phoff ph ph11
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/r02y_tests.txt 2>&1; tail -2 gpurun_out/r02y_tests.txt
+bash scripts/ab.sh "--kernel compact --n 1000000000" 1 u2 u1
+bash scripts/ab.sh "--kernel compact --n 10000000 --family adv" 2 u2 u1
+bash scripts/ab.sh "--kernel compact --n 10000000 --dtype f64 --family adv" 2 u2 u1
+bash scripts/ab.sh "--kernel compact --n 100000000 --family homog" 1 u2 u1
+bash scripts/ab.sh "--kernel compact --n 100000000 --dim 3" 1 u2 u1
