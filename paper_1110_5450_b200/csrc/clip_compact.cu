@@ -110,6 +110,9 @@ __device__ __forceinline__ int atom_add_shared(int* p, int v) {
   asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_addr(p)), "r"(v) : "memory");
   return old;
 }
+__device__ __forceinline__ void atom_or_shared_a(uint32_t a, uint32_t v) {
+  asm volatile("red.shared.or.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+}
 // One thread's global 64-bit fetch-and-add (relaxed, gpu scope).
 __device__ __forceinline__ unsigned long long atom_add_global(unsigned long long* p, unsigned long long v) {
   unsigned long long old;
@@ -676,7 +679,8 @@ template <typename T, class Op, bool INDEX> struct PackedShape {
   static constexpr size_t kRegion = (size_t)BATCH * IN;               // elements per warp region
   // staged tiles (the copy-out lags NBUF-1 tiles): the knob, or fewer when they do not fit
   static constexpr size_t kPerBuf = (size_t)W * (kRegion * sizeof(T) + (INDEX ? BATCH : 0));
-  static constexpr size_t kFixed = (size_t)W * (BATCH / 32 + 1) * 4 + ((size_t)4 << (2 * V)) + (INDEX ? (size_t)W * BATCH : 0);
+  static constexpr size_t kFixed =
+      (size_t)W * (BATCH / 32 + 1) * 4 + ((size_t)4 << (2 * V)) + (size_t)W * BATCH + (INDEX ? (size_t)W * BATCH : 0);
   static constexpr int NBUF = (size_t)K.nbuf * kPerBuf + kFixed <= kMaxSmemPerBlock
                                   ? K.nbuf
                                   : (int)((kMaxSmemPerBlock - kFixed) / kPerBuf);
@@ -685,7 +689,8 @@ template <typename T, class Op, bool INDEX> struct PackedShape {
   static constexpr int VBW = BATCH / 32 + 1;
   static constexpr size_t kVbOff = kStageBytes;                       // [W][VBW] u32
   static constexpr size_t kLutOff = kVbOff + (size_t)W * VBW * 4;     // [2^(2V)] u32: flags of (keep, bits)
-  static constexpr size_t kIdxOff = kLutOff + ((size_t)4 << (2 * V)); // [W][BATCH] list -> local index (INDEX)
+  static constexpr size_t kExcOff = kLutOff + ((size_t)4 << (2 * V)); // [W][BATCH] u8 deferred list positions
+  static constexpr size_t kIdxOff = kExcOff + (size_t)W * BATCH;      // [W][BATCH] list -> local index (INDEX)
   static constexpr size_t kLixOff = kIdxOff + (INDEX ? (size_t)W * BATCH : 0);  // [NBUF][W][BATCH] staged indices
   static constexpr size_t kSmemBytes = kLixOff + (INDEX ? (size_t)NBUF * W * BATCH : 0);
   static constexpr int kThreads = (W + 1) * 32;
@@ -835,6 +840,7 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
   const uint32_t lidx_a = sbase + (uint32_t)S::kIdxOff + warp * BATCH;    // list position -> local index (INDEX)
   const uint32_t vb_a = sbase + (uint32_t)S::kVbOff + warp * S::VBW * 4;  // visible bits of the list
   const uint32_t lut_a = sbase + (uint32_t)S::kLutOff;
+  const uint32_t exc_a = sbase + (uint32_t)S::kExcOff + warp * BATCH;  // deferred (exceptional) list positions
   const uint32_t mbt_a = smem_addr(mb_tile), mbc_a = smem_addr(mb_cnt), mbp_a = smem_addr(mb_pre);
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t full_tiles = n / BT;  // tiles whose every batch is full
@@ -1023,6 +1029,27 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
     int rank = 0;
     const uint32_t slix = INDEX ? sbase + (uint32_t)(S::kLixOff + ((size_t)b * W + warp) * BATCH) : 0u;
     int p0 = 0;
+    // Deferral (CLIPSEG_PK_DEFER): the first round holding a row outside the fast path's range
+    // switches the batch to deferred mode — from there on a fast row's result stays at its
+    // list position (visible bit in the bitmap) and an exceptional row's position is queued;
+    // the queue is then clipped by the rules in dense rounds and the rows from `dstart` on
+    // are compacted to their ranks.  Warps with a few exceptional rows thus run the fast
+    // path and the rules each on full rounds instead of both on every round.
+    constexpr bool DEFER = CLIPSEG_PK_DEFER != 0;
+    bool deferred = false;
+    int dstart = 0, nexc = 0;
+    // one row in deferred mode: the fast path, or the queue
+    auto defer_one = [&](int p, bool act, const T (&row)[IN], bool fok) -> bool {
+      T res[OUT];
+      bool vis = false, done = false;
+      if (fok) done = Op::fast_try(row, w, res, vis);
+      const bool q = act && !done;
+      const unsigned qm = __ballot_sync(0xFFFFFFFFu, q);
+      if (q) sts_u8(exc_a + nexc + __popc(qm & lt_mask), (uint32_t)p);
+      nexc += __popc(qm);
+      if (act && done) sts_row<T, OUT>(region + p * ROWB, res);
+      return act && done && vis;
+    };
     if constexpr (S::K.ilp >= 2) {  // (this instantiation's knob)
     for (; nkept - p0 > 32; p0 += 64) {
       const int pa = p0 + lane, pb = p0 + 32 + lane;
@@ -1034,6 +1061,23 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       const uint32_t ida = INDEX ? lds_u8(lidx_a + pa) : 0u, idb = INDEX ? lds_u8(lidx_a + pbr) : 0u;
       T qa[OUT], qb[OUT];
       bool va, vb;
+      if constexpr (DEFER) {
+        const bool fa = Op::fast_ok(ra, w), fb = Op::fast_ok(rb, w);
+        if (deferred || !__all_sync(0xFFFFFFFFu, fa & fb)) {
+          if (!deferred) {
+            deferred = true;
+            dstart = p0;
+          }
+          __syncwarp();
+          const bool wa = defer_one(pa, true, ra, fa), wb = defer_one(pb, actb, rb, fb);
+          const unsigned ma = __ballot_sync(0xFFFFFFFFu, wa), mb = __ballot_sync(0xFFFFFFFFu, wb);
+          if (lane == 0) {  // visible bits of the fast rows; the queued rows' bits are set later
+            sts_u32(vb_a + 4 * (p0 >> 5), ma);
+            sts_u32(vb_a + 4 * (p0 >> 5) + 4, mb);
+          }
+          continue;
+        }
+      }
 #ifdef CLIPSEG_ABL_NOMATH  // ablation builds only: the framework without the clip
       for (int c = 0; c < OUT; ++c) { qa[c] = ra[c]; qb[c] = rb[c]; }
       va = ra[0] < ra[2]; vb = rb[0] < rb[2];
@@ -1073,6 +1117,20 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       lds_row<T, IN>(region + pr * ROWB, row);
       const uint32_t id = INDEX ? lds_u8(lidx_a + pr) : 0u;
       T res[OUT];
+      if constexpr (DEFER) {
+        const bool fo = Op::fast_ok(row, w);
+        if (deferred || !__all_sync(0xFFFFFFFFu, fo)) {
+          if (!deferred) {
+            deferred = true;
+            dstart = p0;
+          }
+          __syncwarp();
+          const bool wv = defer_one(p, act, row, fo);
+          const unsigned m = __ballot_sync(0xFFFFFFFFu, wv);
+          if (lane == 0) sts_u32(vb_a + 4 * (p0 >> 5), m);
+          continue;
+        }
+      }
 #ifdef CLIPSEG_ABL_NOMATH
       for (int c = 0; c < OUT; ++c) res[c] = row[c];
       const bool vis = (row[0] < row[2]) & act;
@@ -1089,6 +1147,40 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       }
       if (FLAGS && lane == 0) sts_u32(vb_a + 4 * (p0 >> 5), m);
       rank += __popc(m);
+    }
+    if (DEFER && deferred) {
+      __syncwarp();
+      // pass B: the queued rows, by the rules, 32 per round (their results back in place)
+      for (int e0 = 0; e0 < nexc; e0 += 32) {
+        const int e = e0 + lane;
+        const bool act = e < nexc;
+        const int p = (int)lds_u8(exc_a + (act ? e : e0));
+        T row[IN], res[OUT];
+        lds_row<T, IN>(region + p * ROWB, row);
+        const bool vis = Op::exact(row, w, res);
+        if (act) {
+          sts_row<T, OUT>(region + p * ROWB, res);
+          if (vis) atom_or_shared_a(vb_a + 4 * (p >> 5), 1u << (p & 31));
+        }
+      }
+      __syncwarp();
+      // pass C: rows dstart.. to their ranks, in order (rank <= position: in place)
+      for (int q0 = dstart; q0 < nkept; q0 += 32) {
+        const int p = q0 + lane;
+        const bool act = p < nkept;
+        T row[OUT];  // results (OUT elements) sit at the rows' list positions
+        if (act) lds_row<T, OUT>(region + p * ROWB, row);
+        const bool vis = act && ((lds_u32(vb_a + 4 * (q0 >> 5)) >> lane) & 1u);
+        const uint32_t id = (INDEX && act) ? lds_u8(lidx_a + p) : 0u;
+        __syncwarp();
+        const unsigned m = __ballot_sync(0xFFFFFFFFu, vis);
+        if (vis) {
+          const int r = rank + __popc(m & lt_mask);
+          sts_row<T, OUT>(region + r * ROWB, row);
+          if (INDEX) sts_u8(slix + r, id);
+        }
+        rank += __popc(m);
+      }
     }
     if (lane == 0) s_cnt[b][warp] = rank;
     __syncwarp();

@@ -39,6 +39,16 @@ template <typename T, int D> struct BoxOp {  // axis-aligned closed box, D = 2, 
                                                   T (&Qa)[OUT], T (&Qb)[OUT], bool& va, bool& vb) {
     clip_kept2<T, D, false>(Pa, Pb, w, Qa, Qb, va, vb);
   }
+  // deferred exceptional segments: the fast path's range test, the fast path alone (false:
+  // the segment needs the rules) and the rules alone
+  static __device__ __forceinline__ bool fast_ok(const T (&P)[IN], const Params& w) { return box_fast_ok<T, D>(P, w); }
+  static __device__ __forceinline__ bool fast_try(const T (&P)[IN], const Params& w, T (&Q)[OUT], bool& vis) {
+    vis = clip_fast<T, D, false, true>(P, w, Q);
+    return true;
+  }
+  static __device__ __forceinline__ bool exact(const T (&P)[IN], const Params& w, T (&Q)[OUT]) {
+    return clip_exact<T, D>(P, w, Q);
+  }
 };
 struct NoParams {
   int unused;
@@ -79,6 +89,17 @@ template <typename T, bool NDC> struct HomogOp {  // NEXT-1: homogeneous clip sp
   static __device__ __forceinline__ void clip_two(const T (&Pa)[IN], const T (&Pb)[IN], const Params&, T (&Qa)[OUT],
                                                   T (&Qb)[OUT], bool& va, bool& vb) {
     homog_kept2<T, NDC>(Pa, Pb, Qa, Qb, va, vb);
+  }
+  static __device__ __forceinline__ bool fast_ok(const T (&P)[IN], const Params&) { return homog_fast_ok<T>(P); }
+  static __device__ __forceinline__ bool fast_try(const T (&P)[IN], const Params&, T (&Q)[OUT], bool& vis) {
+    bool ok = true;
+    T q[8];
+    vis = homog_fast<T, true>(P, q, ok);
+    if (ok) homog_emit<T, false, NDC>(q, vis, Q);
+    return ok;
+  }
+  static __device__ __forceinline__ bool exact(const T (&P)[IN], const Params&, T (&Q)[OUT]) {
+    return homog_segment<T, false, NDC>(P, Q);
   }
 };
 
@@ -299,6 +320,9 @@ template <typename T, class Op> __host__ __device__ constexpr bool compact_packe
 struct PackedKnobs {
   int warps, pw, nbuf, ilp;
 };
+#ifndef CLIPSEG_PK_DEFER
+#define CLIPSEG_PK_DEFER 0  // 1: segments outside the fast path's range clipped in dense rounds of their own (C3 fp32 0.238 -> 0.211 ms at 1e7, but the headline 5.65 -> 6.18 ms and homogeneous 1.17 -> 1.77 ms: off)
+#endif
 #ifndef CLIPSEG_PK3_ILP
 #define CLIPSEG_PK3_ILP 1
 #endif
