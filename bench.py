@@ -694,14 +694,42 @@ def run_next4(torch, clipseg, synth, dev, stream, n=1 << 28, steps=20):
     wout, wflags = int_oracle.clip_segments_i32(hp, len(idx), lo, hi)
     ok = bool(np.array_equal(flags[ti].cpu().numpy(), wflags)) and bool(np.array_equal(out[:, ti].cpu().numpy(), wout))
     vis = float((flags == 1).sum().item()) / n
-    del planes, out, flags
+    # the compacting variant (same rules): visible rows in input order, flags 0/1/2
+    del out
+    bufs = clipseg.CompactBuffers(n, 2, torch.int32, dev, with_flags=True)
+    for _ in range(3):
+        clipseg.clip_int_compact(planes, n, lo, hi, bufs=bufs, stream=stream)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for a, b in ev:
+        a.record(stream)
+        clipseg.clip_int_compact(planes, n, lo, hi, bufs=bufs, stream=stream)
+        b.record(stream)
+    torch.cuda.synchronize()
+    ms_c = statistics.median(a.elapsed_time(b) for a, b in ev)
+    cnt = int(bufs.count.item())
+    alg_c = n * (16 + 1) + cnt * 16
+    # parity of the compacted rows: sampled visible rows found through the flags' prefix sum
+    cfl = bufs.flags[:n]
+    okc = bool(np.array_equal(cfl[ti].cpu().numpy(), wflags)) and cnt == int((flags == 1).sum().item())
+    pos = torch.cumsum(cfl == 1, 0, dtype=torch.int64) - 1
+    vrows = np.nonzero(wflags == 1)[0]
+    got = bufs.out[:, pos[ti[torch.from_numpy(vrows).to(dev)]]].cpu().numpy()
+    okc = okc and bool(np.array_equal(got, wout[:, vrows]))
+    del planes, flags, bufs, pos, cfl
     return {"workload": f"NEXT-4: int32 2D segments, exact clip, {n} segments, endpoints uniform on [-{S // 2}, "
                         f"{3 * S // 2})^2, window [0, {S - 1}]^2 (SURVEY §8(f))",
             "value": n / (ms / 1e3), "unit": "segments/s", "ms": ms, "visible_fraction": vis,
             "roofline": {"bound": "hbm", "achieved": alg / (ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": alg / (ms / 1e3) / 1e9 / peak, "kernel": "clip_int_kernel",
                          "alg_bytes_per_launch": alg},
-            "parity": f"{'ok' if ok else 'MISMATCH'}: {len(idx)} sampled rows bit-exact vs the exact-rational oracle"}
+            "parity": f"{'ok' if ok else 'MISMATCH'}: {len(idx)} sampled rows bit-exact vs the exact-rational oracle",
+            "compact": {"value": n / (ms_c / 1e3), "unit": "segments/s", "ms": ms_c,
+                        "roofline": {"bound": "hbm", "achieved": alg_c / (ms_c / 1e3) / 1e9, "peak": peak,
+                                     "unit": "GB/s", "frac": alg_c / (ms_c / 1e3) / 1e9 / peak,
+                                     "kernel": "clip_compact_packed_kernel<int,IntOp>", "alg_bytes_per_launch": alg_c},
+                        "parity": f"{'ok' if okc else 'MISMATCH'}: flags of {len(idx)} sampled rows and their "
+                                  "compacted rows bit-exact vs the oracle, count = visible flags"}}
 
 
 def run_next3(torch, clipseg, dev, stream, nframes=296, steps=3):

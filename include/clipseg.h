@@ -209,6 +209,19 @@ typedef struct { int32_t lo[2], hi[2]; } clip_window_i32;
 int clip_segments_i32(const int32_t* in, int64_t ld_in, int64_t n, const clip_window_i32* win, int32_t* out,
                       int64_t ld_out, uint8_t* flags, void* stream);
 
+/* Compacting variant of the int32 clip (NEXT-4 widening; same rules I1-I6): rows [0, count)
+ * of out hold the visible segments' clipped endpoints in increasing input index (rows >= count
+ * are not written); out_index (nullable, int64[count]) = index_base + input index; flags
+ * (nullable, n bytes) 1 visible / 0 invisible / 2 out of range, as clip_segments_i32; d_count:
+ * one int64 in device memory; workspace: clip_compact_workspace_bytes(n) bytes, zero-filled
+ * before its first use and left zero-filled by every call (as the float compacting calls).
+ * out must not overlap in; same window, alignment and status rules as clip_segments_i32.
+ * Results are bit-identical to the exact-rational oracle's visible rows in order. */
+int clip_segments_compact_i32(const int32_t* in, int64_t ld_in, int64_t n, const clip_window_i32* win,
+                              int32_t* out, int64_t ld_out, int64_t* out_index, int64_t index_base,
+                              uint8_t* flags, int64_t* d_count, void* workspace, size_t workspace_bytes,
+                              void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -66,6 +66,9 @@ def _load():
         f.restype = ctypes.c_int
     L.clip_segments_i32.argtypes = [P, I64, I64, ctypes.POINTER(clip_window_i32), P, I64, U8P, P]
     L.clip_segments_i32.restype = ctypes.c_int
+    L.clip_segments_compact_i32.argtypes = [P, I64, I64, ctypes.POINTER(clip_window_i32), P, I64, P, I64, U8P, P, P,
+                                            SZ, P]
+    L.clip_segments_compact_i32.restype = ctypes.c_int
     L.clip_tof_range_phi_f32.argtypes = [P, P, I64, I64, P, P, U8P, P, P]
     L.clip_tof_range_phi_f32.restype = ctypes.c_int
     L.clip_cluster_workspace_bytes.argtypes = [I64, ctypes.c_int, ctypes.c_int]
@@ -98,6 +101,7 @@ clip_segments_compact_host_f32 = _lib.clip_segments_compact_host_f32
 clip_segments_compact_host_f64 = _lib.clip_segments_compact_host_f64
 clip_tof_range_phi_f32 = _lib.clip_tof_range_phi_f32
 clip_segments_i32 = _lib.clip_segments_i32
+clip_segments_compact_i32 = _lib.clip_segments_compact_i32
 clip_cluster_workspace_bytes = _lib.clip_cluster_workspace_bytes
 clip_cluster_frames = _lib.clip_cluster_frames
 clip_homog_segments_f32 = _lib.clip_homog_segments_f32
@@ -110,7 +114,7 @@ EXPORTED = ["clip_plane_stride", "clip_status_string", "clip_segments_f32", "cli
             "clip_shard_offsets", "clip_host_staging_bytes", "clip_segments_compact_host_f32",
             "clip_segments_compact_host_f64", "clip_homog_segments_f32", "clip_homog_segments_f64",
             "clip_homog_segments_compact_f32", "clip_homog_segments_compact_f64", "clip_tof_range_phi_f32",
-            "clip_cluster_workspace_bytes", "clip_cluster_frames", "clip_segments_i32"]
+            "clip_cluster_workspace_bytes", "clip_cluster_frames", "clip_segments_i32", "clip_segments_compact_i32"]
 
 
 class ClipError(RuntimeError):
@@ -298,6 +302,23 @@ def clip_int(planes, n, lo, hi, out=None, flags=None, want_flags=True, stream=No
                              flags.data_ptr() if flags is not None else None, _stream(stream)),
            "clip_segments_i32")
     return out, flags
+
+
+def clip_int_compact(planes, n, lo, hi, bufs: CompactBuffers | None = None, with_index=False, with_flags=False,
+                     index_base=0, stream=None):
+    """Stable compacting int32 clip (NEXT-4 rules) -> CompactBuffers with int32 out rows [0, count)."""
+    torch = _torch()
+    if planes.dtype != torch.int32 or planes.dim() != 2 or planes.shape[0] != 4 or planes.stride(1) != 1:
+        raise ValueError("clip_int_compact: planes must be an int32 (4, ld) row-major plane view")
+    if bufs is None:
+        bufs = CompactBuffers(n, 2, torch.int32, planes.device, with_index, with_flags)
+    win = clip_window_i32((ctypes.c_int32 * 2)(*lo), (ctypes.c_int32 * 2)(*hi))
+    _check(clip_segments_compact_i32(planes.data_ptr(), planes.stride(0), n, ctypes.byref(win), bufs.out.data_ptr(),
+                                     bufs.out.stride(0), bufs.index.data_ptr() if bufs.index is not None else None,
+                                     index_base, bufs.flags.data_ptr() if bufs.flags is not None else None,
+                                     bufs.count.data_ptr(), bufs.ws.data_ptr(), bufs.ws.numel(), _stream(stream)),
+           "clip_segments_compact_i32")
+    return bufs
 
 
 # ---- NEXT-2: range clip + phi over batched ToF frames ----------------------------------------

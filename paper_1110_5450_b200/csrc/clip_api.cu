@@ -380,6 +380,33 @@ int clip_segments_i32(const int32_t* in, int64_t ld_in, int64_t n, const clip_wi
                                    reinterpret_cast<cudaStream_t>(stream)));
 }
 
+int clip_segments_compact_i32(const int32_t* in, int64_t ld_in, int64_t n, const clip_window_i32* win, int32_t* out,
+                              int64_t ld_out, int64_t* out_index, int64_t index_base, uint8_t* flags,
+                              int64_t* d_count, void* workspace, size_t workspace_bytes, void* stream) {
+  if (n < 0 || !win || !d_count) return CLIP_EINVAL;
+  const int64_t B = (int64_t)1 << 30;
+  for (int k = 0; k < 2; ++k)
+    if (win->lo[k] > win->hi[k] || win->lo[k] < -B || win->hi[k] > B) return CLIP_EINVAL;
+  if (!aligned(d_count, 8)) return CLIP_EALIGN;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (n == 0) return status_of(cudaMemsetAsync(d_count, 0, sizeof(int64_t), s));
+  int st;
+  if ((st = check_planes(in, ld_in, n)) || (st = check_planes(out, ld_out, n))) return st;
+  if (flags && !aligned(flags, 4)) return CLIP_EALIGN;
+  if (out_index && !aligned(out_index, 8)) return CLIP_EALIGN;
+  if (!workspace) return CLIP_EINVAL;
+  if (!aligned(workspace, 16)) return CLIP_EALIGN;
+  if (workspace_bytes < clip_compact_workspace_bytes(n)) return CLIP_ENOSPACE;
+  // out must not overlap in (the kernel reads tiles while others write compacted rows)
+  if (!overlap_ok(in, plane_bytes(4, ld_in, n, 4), out, plane_bytes(4, ld_out, n, 4), false)) return CLIP_EINVAL;
+  const int32_t S = 1 << 14;
+  IntWindow w;
+  w.win = make_int4(win->lo[0], win->lo[1], win->hi[0], win->hi[1]);
+  w.small = win->lo[0] >= -S && win->lo[1] >= -S && win->hi[0] <= S && win->hi[1] <= S;
+  return status_of(launch_compact<int32_t, IntOp>(in, ld_in, n, w, out, ld_out, out_index, index_base, flags, d_count,
+                                                  workspace, s));
+}
+
 size_t clip_cluster_workspace_bytes(int64_t nframes, int height, int width) {
   if (nframes < 0 || height < 1 || width < 1) return 0;
   const int64_t part = cluster_part_frames(nframes);  // frames per launch

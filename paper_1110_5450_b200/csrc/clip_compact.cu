@@ -723,8 +723,28 @@ __device__ __forceinline__ void sts_u16(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
 }
 template <typename T, int N>
+__device__ __forceinline__ void sts_row(uint32_t a, const T (&v)[N]);
+template <typename T, int N>
+__device__ __forceinline__ void lds_row(uint32_t a, T (&v)[N]);
+template <int N>
+__device__ __forceinline__ void sts_row(uint32_t a, const int32_t (&v)[N]) {  // int32 rows as their bit patterns
+  float f[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) f[i] = __int_as_float(v[i]);
+  sts_row<float, N>(a, f);
+}
+template <int N>
+__device__ __forceinline__ void lds_row(uint32_t a, int32_t (&v)[N]) {
+  float f[N];
+  lds_row<float, N>(a, f);
+#pragma unroll
+  for (int i = 0; i < N; ++i) v[i] = __float_as_int(f[i]);
+}
+template <typename T, int N>
 __device__ __forceinline__ void sts_row(uint32_t a, const T (&v)[N]) {
-  if constexpr (sizeof(T) == 4 && N % 4 == 0) {  // 16-byte rows: 128-bit stores
+  if constexpr (std::is_same<T, int32_t>::value) {
+    sts_row<N>(a, v);
+  } else if constexpr (sizeof(T) == 4 && N % 4 == 0) {  // 16-byte rows: 128-bit stores
 #pragma unroll
     for (int i = 0; i < N; i += 4)
       asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a + 4 * i), "f"(v[i]), "f"(v[i + 1]),
@@ -744,7 +764,9 @@ __device__ __forceinline__ void sts_row(uint32_t a, const T (&v)[N]) {
 }
 template <typename T, int N>
 __device__ __forceinline__ void lds_row(uint32_t a, T (&v)[N]) {
-  if constexpr (sizeof(T) == 4 && N % 4 == 0) {
+  if constexpr (std::is_same<T, int32_t>::value) {
+    lds_row<N>(a, v);
+  } else if constexpr (sizeof(T) == 4 && N % 4 == 0) {
 #pragma unroll
     for (int i = 0; i < N; i += 4)
       asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -947,11 +969,12 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
     const int rem = batch_rem(tile);
     if (warp == 0 && lane == 0) CLIP_TRACE(tile, 1, trace_now());
     // ---- phase 1: R3, and the kept rows listed in segment order
-    unsigned keep[PW];
+    unsigned keep[PW], oor[PW];
     unsigned cnt = 0;  // kept per sub-tile, byte j
 #pragma unroll
     for (int j = 0; j < PW; ++j) {
       const int o = j * SUB + lane * V;
+      oor[j] = FLAGS ? Op::template oor<T, IN, V>(cur[j]) : 0u;  // flag 2 segments (NEXT-4 I6), not kept
       keep[j] = Op::template keep<V>(cur[j], w, kparams);
       if (rem < BATCH) keep[j] &= (o >= rem) ? 0u : (o + V <= rem ? (1u << V) - 1u : (1u << (rem - o)) - 1u);
       cnt |= (unsigned)__popc(keep[j]) << (8 * j);
@@ -1193,7 +1216,8 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
         const int o = j * SUB + lane * V;
         const uint32_t wa = vb_a + 4 * (kbase[j] >> 5);
         const uint32_t run = __funnelshift_r(lds_u32(wa), lds_u32(wa + 4), kbase[j] & 31) & ((1u << V) - 1u);
-        const uint32_t f = lds_u32(lut_a + 4 * ((keep[j] << V) | run));
+        uint32_t f = lds_u32(lut_a + 4 * ((keep[j] << V) | run));
+        if constexpr (V == 4) f |= ((oor[j] * 0x204081u) & 0x01010101u) << 1;  // out of range -> 2
         if (rem == BATCH || o + V <= rem) {
           if constexpr (V == 4) *reinterpret_cast<uint32_t*>(fl + o) = f;
           else *reinterpret_cast<uint16_t*>(fl + o) = (uint16_t)f;
@@ -1345,6 +1369,7 @@ INST(float, HomF)
 INST(float, HomFN)
 INST(double, HomD)
 INST(double, HomDN)
+INST(int32_t, IntOp)
 #undef INST
 
 }  // namespace clipseg

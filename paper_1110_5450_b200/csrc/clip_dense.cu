@@ -92,11 +92,9 @@ template <typename T, class Op>
 cudaError_t launch_dense(const T* in, int64_t ld_in, int64_t n, const typename Op::Params& w, T* out,
                          int64_t ld_out, uint8_t* flags, cudaStream_t s) {
   constexpr int V = Vec16<T>::N, NT = 256;
-  static int blocks_per_sm = 0;  // cached device attribute
-  if (!blocks_per_sm) {
-    cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, clip_dense_kernel<T, Op>, NT, 0);
-    if (e != cudaSuccess || blocks_per_sm < 1) blocks_per_sm = 1;
-  }
+  int blocks_per_sm = 0;  // per device, cached (kernel_occupancy)
+  cudaError_t e = kernel_occupancy((const void*)clip_dense_kernel<T, Op>, NT, 0, &blocks_per_sm);
+  if (e != cudaSuccess) return e;
   const int64_t ngroups = (n + V - 1) / V;
   const int64_t want = (ngroups + NT - 1) / NT;
   const int64_t cap = (int64_t)device_sm_count() * blocks_per_sm;

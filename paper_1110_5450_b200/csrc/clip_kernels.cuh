@@ -3,7 +3,9 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <type_traits>
 
+#include "clip_int_math.cuh"
 #include "clip_math.cuh"
 
 namespace clipseg {
@@ -11,7 +13,13 @@ namespace clipseg {
 // A clip operation as the kernels see it: IN input planes, OUT output planes per segment,
 // the per-call parameters, and the group clip of V segments (returns the visible bits;
 // NAN_FILL writes R8's qNaN into invisible rows).
-template <typename T, int D> struct BoxOp {  // axis-aligned closed box, D = 2, 3 (rules R1..R10)
+// The packed compacting kernel's optional third flag value: ops whose rules give flag 2 ("out
+// of range", NEXT-4 I6) report those segments here (bit v); every other op reports none.
+struct NoOutOfRange {
+  template <typename T, int IN, int V>
+  static __device__ __forceinline__ unsigned oor(const T (&)[IN][V]) { return 0u; }
+};
+template <typename T, int D> struct BoxOp : NoOutOfRange {  // axis-aligned closed box, D = 2, 3 (rules R1..R10)
   static constexpr int IN = 2 * D, OUT = 2 * D;
   static constexpr int GV = 4;  // whole groups (V <= 4)
   typedef Window<T, D> Params;
@@ -53,6 +61,65 @@ template <typename T, int D> struct BoxOp {  // axis-aligned closed box, D = 2, 
 struct NoParams {
   int unused;
 };
+
+// NEXT-4: int32 2D segments against a closed integer window, exact rules
+// I1-I6 (clip_int_math.cuh).  Packed compacting kernel only (the dense call has its own kernel).
+struct IntWindow {
+  int4 win;   // lo.x, lo.y, hi.x, hi.y
+  int small;  // every window bound within [-2^14, 2^14]: the 32-bit path is allowed
+};
+struct IntOp {
+  typedef int32_t T;
+  static constexpr int IN = 4, OUT = 4;
+  typedef IntWindow Params;
+  struct KeepParams {
+    int unused;
+  };
+  static __device__ __forceinline__ KeepParams keep_params(const Params&) { return KeepParams{0}; }
+  // kept: every coordinate within I1's range and not trivially rejected (I2's both-outside test,
+  // exact on integers); out-of-range segments are not kept and get flag 2 (oor)
+  template <int V>
+  static __device__ __forceinline__ unsigned keep(const int32_t (&pl)[IN][V], const Params& w, const KeepParams&) {
+    unsigned m = 0;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+      const int32_t x0 = pl[0][v], y0 = pl[1][v], x1 = pl[2][v], y1 = pl[3][v];
+      const bool rej = (max(x0, x1) < w.win.x) | (min(x0, x1) > w.win.z) | (max(y0, y1) < w.win.y) |
+                       (min(y0, y1) > w.win.w);
+      m |= ((!rej & in_range(x0, y0, x1, y1)) ? 1u : 0u) << v;
+    }
+    return m;
+  }
+  template <typename TT, int IIN, int V>
+  static __device__ __forceinline__ unsigned oor(const TT (&pl)[IIN][V]) {
+    unsigned m = 0;
+#pragma unroll
+    for (int v = 0; v < V; ++v) m |= (in_range(pl[0][v], pl[1][v], pl[2][v], pl[3][v]) ? 0u : 1u) << v;
+    return m;
+  }
+  static __device__ __forceinline__ bool in_range(int32_t x0, int32_t y0, int32_t x1, int32_t y1) {
+    // |c| <= 2^30 for all four: biased into [0, 2^31] in unsigned arithmetic
+    const uint32_t b = (uint32_t)intclip::kCoordMax;
+    const uint32_t m = max(max((uint32_t)x0 + b, (uint32_t)y0 + b), max((uint32_t)x1 + b, (uint32_t)y1 + b));
+    return m <= 2u * b;
+  }
+  static __device__ __forceinline__ bool clip_one(const int32_t (&P)[IN], const Params& w, int32_t (&Q)[OUT]) {
+    return intclip::clip_int_one(P[0], P[1], P[2], P[3], w.win, w.small != 0, Q) == 1u;
+  }
+  static __device__ __forceinline__ void clip_two(const int32_t (&Pa)[IN], const int32_t (&Pb)[IN], const Params& w,
+                                                  int32_t (&Qa)[OUT], int32_t (&Qb)[OUT], bool& va, bool& vb) {
+    va = clip_one(Pa, w, Qa);
+    vb = clip_one(Pb, w, Qb);
+  }
+  static __device__ __forceinline__ bool fast_ok(const int32_t (&)[IN], const Params&) { return true; }
+  static __device__ __forceinline__ bool fast_try(const int32_t (&P)[IN], const Params& w, int32_t (&Q)[OUT], bool& vis) {
+    vis = clip_one(P, w, Q);
+    return true;
+  }
+  static __device__ __forceinline__ bool exact(const int32_t (&P)[IN], const Params& w, int32_t (&Q)[OUT]) {
+    return clip_one(P, w, Q);
+  }
+};
 #ifndef CLIPSEG_HOMOG_GV_F32
 #define CLIPSEG_HOMOG_GV_F32 2      // segments per group_chunked call, fp32 homogeneous output
 #endif
@@ -62,7 +129,7 @@ struct NoParams {
 #ifndef CLIPSEG_HOMOG_GV_F64
 #define CLIPSEG_HOMOG_GV_F64 2
 #endif
-template <typename T, bool NDC> struct HomogOp {  // NEXT-1: homogeneous clip space (rules H1..H10)
+template <typename T, bool NDC> struct HomogOp : NoOutOfRange {  // NEXT-1: homogeneous clip space (rules H1..H10)
   static constexpr int IN = 8, OUT = NDC ? 6 : 8;
   // Segments clipped per call: the six-plane rules of 4 segments at once need more than 128
   // registers (spills at 80: 168 B); chunks of 2 (1 with the NDC divides) do not, measured
@@ -311,7 +378,8 @@ template <typename T, class Op> __host__ __device__ constexpr bool compact_packe
   return (compact_headline<T, Op>() && CLIPSEG_PACKED_F32_2D != 0) ||
          (sizeof(T) == 4 && Op::IN == 6 && Op::OUT == 6 && CLIPSEG_PACKED_F32_3D != 0) ||
          (sizeof(T) == 4 && Op::IN == 8 && CLIPSEG_PACKED_F32_H != 0) ||
-         (sizeof(T) == 8 && Op::IN == 4 && Op::OUT == 4 && CLIPSEG_PACKED_F64_2D != 0);
+         (sizeof(T) == 8 && Op::IN == 4 && Op::OUT == 4 && CLIPSEG_PACKED_F64_2D != 0) ||
+         std::is_same<Op, IntOp>::value;
 }
 // (compute warps, sub-tiles per warp batch, staged tiles, kept rows per lane per round),
 // measured (scripts/ab.sh): two rows per lane pay for 2D fp32 (5.9 -> 5.6 ms at 1e9) and

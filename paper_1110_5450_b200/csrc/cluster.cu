@@ -397,11 +397,9 @@ static cudaError_t launch_cluster_part(const float* z, const float* phi, const u
   w.counts = reinterpret_cast<int*>(take(64));
   const cudaError_t e = cudaMemsetAsync(w.counts, 0, 64, s);
   if (e != cudaSuccess) return e;
-  static int blocks_per_sm = 0;
-  if (!blocks_per_sm) {
-    const cudaError_t e2 = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, cluster_kernel, 256, 0);
-    if (e2 != cudaSuccess || blocks_per_sm < 1) blocks_per_sm = 1;
-  }
+  int blocks_per_sm = 0;  // per device, cached (kernel_occupancy)
+  const cudaError_t e2 = kernel_occupancy((const void*)cluster_kernel, 256, 0, &blocks_per_sm);
+  if (e2 != cudaSuccess) return e2;
 #ifndef CLIPSEG_CLUSTER_PIX_PER_BLOCK
 #define CLIPSEG_CLUSTER_PIX_PER_BLOCK 512  // pixels per block (128..2048 measured alike; 8192 slower)
 #endif

@@ -149,11 +149,9 @@ cudaError_t launch_tof_range_phi(const float* d, const float* I, int64_t n, int6
     if (e != cudaSuccess) return e;
   }
   constexpr int NT = 256;
-  static int blocks_per_sm = 0;  // cached device attribute
-  if (!blocks_per_sm) {
-    const cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, tof_range_phi_kernel, NT, 0);
-    if (e != cudaSuccess || blocks_per_sm < 1) blocks_per_sm = 1;
-  }
+  int blocks_per_sm = 0;  // per device, cached (kernel_occupancy)
+  const cudaError_t eo = kernel_occupancy((const void*)tof_range_phi_kernel, NT, 0, &blocks_per_sm);
+  if (eo != cudaSuccess) return eo;
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
   const int64_t want = (nchunks * 32 + NT - 1) / NT;
   const int64_t cap = (int64_t)device_sm_count() * blocks_per_sm;  // persistent: one resident wave

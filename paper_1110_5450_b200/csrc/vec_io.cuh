@@ -12,6 +12,12 @@ template <> struct Vec16<float> {
   static __device__ __forceinline__ void unpack(const float4& v, float (&a)[4]) { a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w; }
   static __device__ __forceinline__ float4 pack(const float (&a)[4]) { return make_float4(a[0], a[1], a[2], a[3]); }
 };
+template <> struct Vec16<int32_t> {
+  typedef int4 type;
+  static constexpr int N = 4;
+  static __device__ __forceinline__ void unpack(const int4& v, int32_t (&a)[4]) { a[0] = v.x; a[1] = v.y; a[2] = v.z; a[3] = v.w; }
+  static __device__ __forceinline__ int4 pack(const int32_t (&a)[4]) { return make_int4(a[0], a[1], a[2], a[3]); }
+};
 template <> struct Vec16<double> {
   typedef double2 type;
   static constexpr int N = 2;

@@ -103,3 +103,50 @@ def test_fullsize_sampled(torch, cs):
     wout, wflags = O.clip_segments_i32(planes, n, *SCREEN, idx=idx)
     assert np.array_equal(flags[idx], wflags)
     assert np.array_equal(out[:, idx], wout)
+
+
+# ---- the compacting int32 clip (NEXT-4 widening): visible rows in input order, flags 0/1/2 ----
+def check_compact(torch, cs, planes, n, lo, hi, index_base=0):
+    wout, wflags = O.clip_segments_i32(planes, n, lo, hi)
+    vis = np.nonzero(wflags == 1)[0]
+    b = cs.clip_int_compact(torch.from_numpy(planes).cuda(), n, lo, hi, with_index=True, with_flags=True,
+                            index_base=index_base)
+    torch.cuda.synchronize()
+    cnt = int(b.count.item())
+    assert cnt == len(vis)
+    flags = b.flags.cpu().numpy()[:n]
+    bad = np.nonzero(flags != wflags)[0]
+    assert bad.size == 0, (bad[:10], flags[bad[:10]], wflags[bad[:10]], planes[:, bad[:3]])
+    assert np.array_equal(b.index.cpu().numpy()[:cnt], vis + index_base)
+    got = b.out.cpu().numpy()[:, :cnt]
+    bad = np.nonzero((got != wout[:, vis]).any(axis=0))[0]
+    assert bad.size == 0, (bad[:10], planes[:, vis[bad[:3]]], got[:, bad[:3]], wout[:, vis[bad[:3]]])
+    assert not b.ws.any().item(), "workspace not left zero-filled"
+    return flags
+
+
+@pytest.mark.parametrize("n", [1, 5, 255, 256, 257, 3839, 3840, 3841, 30001, 200003])
+@pytest.mark.parametrize("mix", ["screen", "edge", "wide", "range", "mixed"])
+def test_compact_parity(torch, cs, n, mix):
+    planes = synth.int_segments_host(2000 + n, n, mix)
+    flags = check_compact(torch, cs, planes, n, *SCREEN, index_base=7)
+    if n > 1000 and mix == "range":
+        assert (flags == 2).any()
+
+
+def test_compact_windows(torch, cs):
+    B = 1 << 30
+    k = 1 << 14
+    planes = synth.int_segments_host(17, 50000, "mixed")
+    for lo, hi in (([-B, -B], [B, B]), ([5, 5], [5, 5]), ([-k, -k], [k, k]), ([-k - 1, 0], [k, k]),
+                   ([-1000, -7], [123456, 999999])):
+        check_compact(torch, cs, planes, 50000, lo, hi)
+
+
+def test_compact_empty_and_none_visible(torch, cs):
+    planes = synth.int_segments_host(5, 4096, "screen")
+    b = cs.clip_int_compact(torch.from_numpy(planes).cuda(), 0, *SCREEN)
+    torch.cuda.synchronize()
+    assert int(b.count.item()) == 0
+    far = np.full((4, 4096), 1 << 20, dtype=np.int32)  # every segment beyond the window
+    check_compact(torch, cs, far, 4000, *SCREEN)
