@@ -179,6 +179,47 @@ StageLayout stage_layout(int dim, int elem, int64_t chunk) {
   return L;
 }
 
+// Streams and events of the pipelined host entry, per host thread and device: a call on
+// another thread gets its own set (the entry stays reentrant), repeated calls reuse it.
+// Created on first use; released when the thread exits.
+struct HostPipe {
+  cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr, sk = nullptr;
+  cudaEvent_t h2d_done[2] = {}, comp_done[2] = {}, d2h_done[2] = {};
+  bool ready = false;
+  ~HostPipe() {
+    if (!ready) return;
+    for (int s = 0; s < 2; ++s) {
+      cudaEventDestroy(h2d_done[s]);
+      cudaEventDestroy(comp_done[s]);
+      cudaEventDestroy(d2h_done[s]);
+    }
+    cudaStreamDestroy(sh);
+    cudaStreamDestroy(sc);
+    cudaStreamDestroy(sd);
+    cudaStreamDestroy(sk);
+  }
+};
+HostPipe* host_pipe() {
+  constexpr int kMaxDev = 64;
+  thread_local HostPipe pipes[kMaxDev];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDev) return nullptr;
+  HostPipe& p = pipes[dev];
+  if (!p.ready) {
+    bool ok = cudaStreamCreateWithFlags(&p.sh, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&p.sc, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&p.sd, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaStreamCreateWithFlags(&p.sk, cudaStreamNonBlocking) == cudaSuccess;
+    for (int s = 0; s < 2 && ok; ++s)
+      ok = cudaEventCreateWithFlags(&p.h2d_done[s], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&p.comp_done[s], cudaEventDisableTiming) == cudaSuccess &&
+           cudaEventCreateWithFlags(&p.d2h_done[s], cudaEventDisableTiming) == cudaSuccess;
+    if (!ok) return nullptr;
+    p.ready = true;
+  }
+  return &p;
+}
+
 template <typename T>
 int compact_host(const T* h_in, int64_t ld_in, int64_t n, const typename WinT<T>::type* win, T* h_out,
                  int64_t ld_out, uint8_t* h_flags, int64_t* h_count, int64_t chunk, void* d_staging,
@@ -199,17 +240,15 @@ int compact_host(const T* h_in, int64_t ld_in, int64_t n, const typename WinT<T>
   char* base = reinterpret_cast<char*>(d_staging);
   auto set_ptr = [&](int s, size_t off) { return base + (size_t)s * L.set_bytes + off; };
 
-  cudaStream_t sh = nullptr, sc = nullptr, sd = nullptr, sk = nullptr;
-  cudaEvent_t h2d_done[2] = {}, comp_done[2] = {}, d2h_done[2] = {};
+  // the pipeline's streams and events, created once per (host thread, device) and reused
+  HostPipe* pipe = host_pipe();
+  bool ok = pipe != nullptr;
+  if (!ok) return CLIP_ECUDA;
+  cudaStream_t sh = pipe->sh, sc = pipe->sc, sd = pipe->sd, sk = pipe->sk;
+  cudaEvent_t* h2d_done = pipe->h2d_done;
+  cudaEvent_t* comp_done = pipe->comp_done;
+  cudaEvent_t* d2h_done = pipe->d2h_done;
   int rc = CLIP_OK;
-  bool ok = cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking) == cudaSuccess &&
-            cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking) == cudaSuccess &&
-            cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking) == cudaSuccess &&
-            cudaStreamCreateWithFlags(&sk, cudaStreamNonBlocking) == cudaSuccess;
-  for (int s = 0; s < 2 && ok; ++s)
-    ok = cudaEventCreateWithFlags(&h2d_done[s], cudaEventDisableTiming) == cudaSuccess &&
-         cudaEventCreateWithFlags(&comp_done[s], cudaEventDisableTiming) == cudaSuccess &&
-         cudaEventCreateWithFlags(&d2h_done[s], cudaEventDisableTiming) == cudaSuccess;
   const int64_t nch = (n + chunk - 1) / chunk;
   int64_t written = 0;
 
@@ -267,15 +306,6 @@ int compact_host(const T* h_in, int64_t ld_in, int64_t n, const typename WinT<T>
     if (sc) cudaStreamSynchronize(sc);
     if (sd) cudaStreamSynchronize(sd);
   }
-  for (int s = 0; s < 2; ++s) {
-    if (h2d_done[s]) cudaEventDestroy(h2d_done[s]);
-    if (comp_done[s]) cudaEventDestroy(comp_done[s]);
-    if (d2h_done[s]) cudaEventDestroy(d2h_done[s]);
-  }
-  if (sh) cudaStreamDestroy(sh);
-  if (sc) cudaStreamDestroy(sc);
-  if (sd) cudaStreamDestroy(sd);
-  if (sk) cudaStreamDestroy(sk);
   if (rc == CLIP_OK) *h_count = written;
   return rc;
 }

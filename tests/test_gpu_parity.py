@@ -174,10 +174,20 @@ def test_host_pipeline(torch, cs, dtype):
     h_in = torch.from_numpy(planes).pin_memory()
     h_out = torch.empty_like(h_in).pin_memory()
     h_flags = torch.empty(n, dtype=torch.uint8).pin_memory()
-    cnt, _ = cs.clip_compact_host(h_in, n, *UNIT[2], h_out, h_flags=h_flags, chunk=300000)
+    cnt, staging = cs.clip_compact_host(h_in, n, *UNIT[2], h_out, h_flags=h_flags, chunk=300000)
     assert cnt == wcnt
     assert np.array_equal(h_flags.numpy(), wflags)
     assert np.array_equal(bits(h_out.numpy()[:, :cnt]), bits(want[:, :cnt]))
+    # again on the same thread (the pipeline's streams and events are reused), a shorter input
+    m = 77777
+    want2, _, wcnt2, wflags2 = oracle.compact(planes[:, :synth.plane_stride(m)].copy(), m, *UNIT[2], 2,
+                                              with_flags=True)
+    h_out.zero_()
+    cnt2, _ = cs.clip_compact_host(h_in[:, :synth.plane_stride(m)].contiguous(), m, *UNIT[2], h_out, h_flags=h_flags,
+                                   chunk=30000, staging=None)
+    assert cnt2 == wcnt2
+    assert np.array_equal(h_flags.numpy()[:m], wflags2)
+    assert np.array_equal(bits(h_out.numpy()[:, :cnt2]), bits(want2[:, :cnt2]))
 
 
 @pytest.mark.parametrize("dtype", [np.float32, np.float64])
