@@ -249,7 +249,7 @@ template <int NSUB, int NBUF>
 __device__ __forceinline__ void tile_scan_warp(int lane, int64_t ntiles, unsigned long long* status,
                                                const int64_t* s_tile, const int (*s_cnt)[NSUB], int (*s_pre)[NSUB],
                                                int64_t* s_prefix, int* s_done, uint64_t* mb_tile, uint64_t* mb_cnt,
-                                               uint64_t* mb_pre, int64_t* s_tileof = nullptr) {
+                                               uint64_t* mb_pre, int64_t* s_tileof = nullptr, bool publish = false) {
   static_assert(NSUB <= 64, "two counts per lane");
   int b = 0;
   unsigned par = 0;  // bit q: parity of the next phase of mb_cnt[q] / mb_pre[q]
@@ -273,6 +273,7 @@ __device__ __forceinline__ void tile_scan_warp(int lane, int64_t ntiles, unsigne
     if (lane < NSUB) s_pre[b][lane] = (incl & 0xFFFF) - c0;
     if (NSUB > 32 && lane + 32 < NSUB) s_pre[b][lane + 32] = (tot & 0xFFFF) + (incl >> 16) - c1;
     const int64_t total = (tot & 0xFFFF) + (tot >> 16);
+    if (publish && lane == 0) st_relaxed(status + tile, kFlagA | (unsigned long long)total);  // the tile aggregate
     if (lane == 0) {
       CLIP_TRACE(tile, 3, trace_now());
       unsigned long long st;
@@ -784,6 +785,10 @@ __device__ __forceinline__ void lds_row(uint32_t a, T (&v)[N]) {
   }
 }
 
+#ifndef CLIPSEG_PK_SCANPUB
+#define CLIPSEG_PK_SCANPUB 0  // 1: the scan warp publishes each aggregate (measured 5.73 -> 11.1 ms: it then waits for its
+                              // prefix before publishing the next tile, serialising the blocks)
+#endif
 #ifndef CLIPSEG_PK_MAXNREG
 #define CLIPSEG_PK_MAXNREG 0  // > 0: register cap instead of the launch bounds (A/B builds)
 #endif
@@ -851,7 +856,8 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
     return;
   }
   if (warp == W) {
-    tile_scan_warp<W, NBUF>(lane, ntiles, status, s_tile, s_cnt, s_pre, s_prefix, s_done, mb_tile, mb_cnt, mb_pre);
+    tile_scan_warp<W, NBUF>(lane, ntiles, status, s_tile, s_cnt, s_pre, s_prefix, s_done, mb_tile, mb_cnt, mb_pre,
+                            nullptr, CLIPSEG_PK_SCANPUB != 0);
     block_exit(ws, lane);
     return;
   }
@@ -1227,13 +1233,14 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
         }
       }
     }
-    // the last compute warp to finish publishes the tile aggregate (flag A)
+    // the last compute warp to finish publishes the tile aggregate (flag A), or the scan warp
+    // does once every count is in (CLIPSEG_PK_SCANPUB)
     int last = 0;
-    if (lane == 0) {
+    if (!CLIPSEG_PK_SCANPUB && lane == 0) {
       __threadfence_block();
       last = atom_add_shared(&s_done[b], 1) == W - 1;
     }
-    last = __shfl_sync(0xFFFFFFFFu, last, 0);
+    if (!CLIPSEG_PK_SCANPUB) last = __shfl_sync(0xFFFFFFFFu, last, 0);
     if (last) {
       __threadfence_block();
       int c = (lane < W) ? ((volatile int*)s_cnt[b])[lane] : 0;
