@@ -694,7 +694,16 @@ template <typename T, class Op, bool INDEX> struct PackedShape {
   static constexpr size_t kIdxOff = kExcOff + (size_t)W * BATCH;      // [W][BATCH] list -> local index (INDEX)
   static constexpr size_t kLixOff = kIdxOff + (INDEX ? (size_t)W * BATCH : 0);  // [NBUF][W][BATCH] staged indices
   static constexpr size_t kSmemBytes = kLixOff + (INDEX ? (size_t)NBUF * W * BATCH : 0);
-  static constexpr int kThreads = (W + 1) * 32;
+  // copy warps: a service warpgroup (the scan warp + COPYW copy warps) copies the staged
+  // batches out, so compute warps neither copy nor wait for offsets (CLIPSEG_PK_COPYW)
+  static constexpr int COPYW = compact_headline<T, Op>() ? CLIPSEG_PK_COPYW : 0;
+  static constexpr int kThreads = (W + 1 + COPYW) * 32;
+  static_assert(COPYW == 0 || ((W % 4) == 0 && ((1 + COPYW) % 4) == 0), "whole warpgroups for setmaxnreg");
+  // the launch allocates the block kLaunchRegs per thread (per-SMSP share, 8-register granules);
+  // setmaxnreg only moves registers inside that pool, so the split must fit it
+  static constexpr int kLaunchRegs = ((16384 / ((((kThreads / 32) + 3) / 4) * 32)) / 8) * 8;
+  static_assert(COPYW == 0 || W * 32 * CLIPSEG_PK_REG_C + (1 + COPYW) * 32 * CLIPSEG_PK_REG_S <= kThreads * kLaunchRegs,
+                "register split exceeds the block's pool (setmaxnreg.inc would never return)");
   static_assert(BATCH <= 256, "local indices are bytes");
   static_assert(OUT <= IN, "rows are written back in place");
   static_assert(kSmemBytes <= kMaxSmemPerBlock, "shared memory");
@@ -816,6 +825,8 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
   __shared__ __align__(8) uint64_t mb_cnt[NBUF];
   __shared__ __align__(8) uint64_t mb_pre[NBUF];
   __shared__ __align__(8) uint64_t mb_tile[kTileRing];
+  __shared__ __align__(8) uint64_t mb_free[NBUF];  // copy warps -> compute warps: buffer copied out
+  constexpr int CW = S::COPYW;
 
   unsigned long long* counter = ws;
   unsigned long long* status = ws + kWsHeaderBytes / 8;
@@ -840,6 +851,8 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       mbar_init(&mb_pre[q], 1);
     }
     for (int q = 0; q < kTileRing; ++q) mbar_init(&mb_tile[q], 1);
+    if (CW)
+      for (int q = 0; q < NBUF; ++q) mbar_init(&mb_free[q], CW);
     if (blockIdx.x != 0) {  // the tiles of iterations 0 and 1
       s_tile[0] = (int64_t)atom_add_global(counter, 1ull);
       s_tile[1] = (int64_t)atom_add_global(counter, 1ull);
@@ -855,12 +868,56 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
     }
     return;
   }
-  if (warp == W) {
-    tile_scan_warp<W, NBUF>(lane, ntiles, status, s_tile, s_cnt, s_pre, s_prefix, s_done, mb_tile, mb_cnt, mb_pre,
-                            nullptr, CLIPSEG_PK_SCANPUB != 0);
-    block_exit(ws, lane);
+  if (warp >= W) {  // ------------------------------------- service warpgroup: scan warp (+ copy warps)
+    // warpgroup register split: the service warps give registers to the compute warps
+    if constexpr (CW > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(CLIPSEG_PK_REG_S));
+    if (warp == W) {
+      tile_scan_warp<W, NBUF>(lane, ntiles, status, s_tile, s_cnt, s_pre, s_prefix, s_done, mb_tile, mb_cnt, mb_pre,
+                              nullptr, CLIPSEG_PK_SCANPUB != 0);
+      block_exit(ws, lane);
+      return;
+    }
+    if constexpr (CW > 0) {  // ---------------------------------------------------- copy warps
+      const int cw = warp - W - 1;
+      const uint32_t sb = smem_addr(smem_raw);
+      int bb = 0;
+      unsigned ppar = 0;
+      for (int64_t kk = 0;; ++kk) {
+        mbar_wait_sleepy(&mb_tile[kk & kRingMask], (uint32_t)((kk / kTileRing) & 1), 128);
+        const int64_t tk = s_tile[kk & kRingMask];
+        if (tk >= ntiles) break;
+        mbar_wait_a(smem_addr(&mb_pre[bb]), (ppar >> bb) & 1u);  // the tile's offsets
+        ppar ^= 1u << bb;
+        const int64_t prefix = s_prefix[bb];
+        for (int w2 = cw; w2 < W; w2 += CW) {
+          const int cnt = s_cnt[bb][w2];
+          const int64_t g0 = prefix + s_pre[bb][w2];
+          const uint32_t reg = sb + (uint32_t)(((size_t)bb * W + w2) * S::kRegion * sizeof(T)) + lane * ROWB;
+          T* dst[OUT];
+#pragma unroll
+          for (int c = 0; c < OUT; ++c) dst[c] = out + c * ld_out + g0 + lane;
+          const uint32_t slix = sb + (uint32_t)(S::kLixOff + ((size_t)bb * W + w2) * BATCH) + lane;
+          const int64_t ib = INDEX ? index_base + tk * BT + (int64_t)w2 * BATCH : 0;
+#pragma unroll
+          for (int q = 0; q < BATCH / 32; ++q) {
+            if (q * 32 >= cnt) break;
+            if (q * 32 + lane < cnt) {
+              T row[IN];
+              lds_row<T, IN>(reg + q * 32 * ROWB, row);
+#pragma unroll
+              for (int c = 0; c < OUT; ++c) __stcs(dst[c] + q * 32, row[c]);
+              if (INDEX) out_index[g0 + q * 32 + lane] = ib + lds_u8(slix + q * 32);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&mb_free[bb]);  // this buffer may be refilled
+        bb = (bb + 1 == NBUF) ? 0 : bb + 1;
+      }
+    }
     return;
   }
+  if constexpr (CW > 0) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(CLIPSEG_PK_REG_C));
 
   // ------------------------------------------------------------------ compute warps
   const typename Op::KeepParams kparams = Op::keep_params(w);
@@ -870,6 +927,8 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
   const uint32_t lut_a = sbase + (uint32_t)S::kLutOff;
   const uint32_t exc_a = sbase + (uint32_t)S::kExcOff + warp * BATCH;  // deferred (exceptional) list positions
   const uint32_t mbt_a = smem_addr(mb_tile), mbc_a = smem_addr(mb_cnt), mbp_a = smem_addr(mb_pre);
+  const uint32_t mbf_a = smem_addr(mb_free);
+  unsigned fpar = 0;  // bit q: parity of the next phase of mb_free[q] (copy-warp mode)
   const unsigned lt_mask = (1u << lane) - 1u;
   const int64_t full_tiles = n / BT;  // tiles whose every batch is full
   const T* lane_in = in + (int64_t)warp * BATCH + lane * V;
@@ -993,6 +1052,12 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
     }
     const unsigned tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
     const unsigned excl = incl - cnt;
+    if constexpr (CW > 0) {
+      if (k >= NBUF) {  // the copy warps are done with this buffer's previous tile
+        mbar_wait_a(mbf_a + 8 * b, (fpar >> b) & 1u);
+        fpar ^= 1u << b;
+      }
+    }
     __syncwarp();  // the previous use of this region (a copy-out) is done
     int before = 0;
     int kbase[PW];  // list position of this lane's first kept segment of sub-tile j
@@ -1079,6 +1144,36 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       if (act && done) sts_row<T, OUT>(region + p * ROWB, res);
       return act && done && vis;
     };
+    if constexpr (S::K.ilp >= 3) {  // NI rows per lane per round (this instantiation's knob)
+      constexpr int NI = S::K.ilp;
+      for (; nkept - p0 > 32 * (NI - 1); p0 += 32 * NI) {
+        T rr[NI][IN], qq[NI][OUT];
+        bool vv[NI], ac[NI];
+        uint32_t id[NI];
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+          const int p = p0 + 32 * i + lane;
+          ac[i] = p < nkept;
+          const int pr = ac[i] ? p : p0 + lane;  // an idle row re-clips the round's first one
+          lds_row<T, IN>(region + pr * ROWB, rr[i]);
+          id[i] = INDEX ? lds_u8(lidx_a + pr) : 0u;
+        }
+        Op::template clip_n<NI>(rr, w, qq, vv);
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+          const bool v = vv[i] & ac[i];
+          const unsigned m = __ballot_sync(0xFFFFFFFFu, v);
+          if (v) {
+            const int r = rank + __popc(m & lt_mask);
+            sts_row<T, OUT>(region + r * ROWB, qq[i]);
+            if (INDEX) sts_u8(slix + r, id[i]);
+          }
+          if (FLAGS && lane == 0) sts_u32(vb_a + 4 * ((p0 >> 5) + i), m);
+          rank += __popc(m);
+        }
+      }
+    }
     if constexpr (S::K.ilp >= 2) {  // (this instantiation's knob)
     for (; nkept - p0 > 32; p0 += 64) {
       const int pa = p0 + lane, pb = p0 + 32 + lane;
@@ -1256,10 +1351,12 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
     if (lane == 0) mbar_arrive_a(mbc_a + 8 * b);
     // copy out iteration k - (NBUF-1), NBUF-1 tiles behind: its offsets are known by now
     b = cb;  // buffer of iteration k + 1 == buffer of iteration k - (NBUF-1)
-    if (early) {
-      while (cq * 32 < ccnt) copy_round();
-    } else if (pend[NBUF - 2] < ntiles) {
-      copy_out(pend[NBUF - 2], b);
+    if constexpr (CW == 0) {
+      if (early) {
+        while (cq * 32 < ccnt) copy_round();
+      } else if (pend[NBUF - 2] < ntiles) {
+        copy_out(pend[NBUF - 2], b);
+      }
     }
 #pragma unroll
     for (int q = NBUF - 2; q > 0; --q) pend[q] = pend[q - 1];
@@ -1267,10 +1364,12 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
     tile = next;
   }
   // drain: the last NBUF-1 iterations are still staged (oldest first)
+  if constexpr (CW == 0) {
 #pragma unroll
-  for (int q = NBUF - 2; q >= 0; --q) {
-    b = (b + 1 == NBUF) ? 0 : b + 1;
-    if (pend[q] < ntiles) copy_out(pend[q], b);
+    for (int q = NBUF - 2; q >= 0; --q) {
+      b = (b + 1 == NBUF) ? 0 : b + 1;
+      if (pend[q] < ntiles) copy_out(pend[q], b);
+    }
   }
 }
 

@@ -47,6 +47,11 @@ template <typename T, int D> struct BoxOp : NoOutOfRange {  // axis-aligned clos
                                                   T (&Qa)[OUT], T (&Qb)[OUT], bool& va, bool& vb) {
     clip_kept2<T, D, false>(Pa, Pb, w, Qa, Qb, va, vb);
   }
+  template <int NI>
+  static __device__ __forceinline__ void clip_n(const T (&P)[NI][IN], const Params& w, T (&Q)[NI][OUT],
+                                                bool (&vis)[NI]) {
+    clip_keptN<T, D, NI>(P, w, Q, vis);
+  }
   // deferred exceptional segments: the fast path's range test, the fast path alone (false:
   // the segment needs the rules) and the rules alone
   static __device__ __forceinline__ bool fast_ok(const T (&P)[IN], const Params& w) { return box_fast_ok<T, D>(P, w); }
@@ -111,6 +116,12 @@ struct IntOp {
     va = clip_one(Pa, w, Qa);
     vb = clip_one(Pb, w, Qb);
   }
+  template <int NI>
+  static __device__ __forceinline__ void clip_n(const int32_t (&P)[NI][IN], const Params& w, int32_t (&Q)[NI][OUT],
+                                                bool (&vis)[NI]) {
+#pragma unroll
+    for (int i = 0; i < NI; ++i) vis[i] = clip_one(P[i], w, Q[i]);
+  }
   static __device__ __forceinline__ bool fast_ok(const int32_t (&)[IN], const Params&) { return true; }
   static __device__ __forceinline__ bool fast_try(const int32_t (&P)[IN], const Params& w, int32_t (&Q)[OUT], bool& vis) {
     vis = clip_one(P, w, Q);
@@ -156,6 +167,10 @@ template <typename T, bool NDC> struct HomogOp : NoOutOfRange {  // NEXT-1: homo
   static __device__ __forceinline__ void clip_two(const T (&Pa)[IN], const T (&Pb)[IN], const Params&, T (&Qa)[OUT],
                                                   T (&Qb)[OUT], bool& va, bool& vb) {
     homog_kept2<T, NDC>(Pa, Pb, Qa, Qb, va, vb);
+  }
+  template <int NI>
+  static __device__ __forceinline__ void clip_n(const T (&P)[NI][IN], const Params&, T (&Q)[NI][OUT], bool (&vis)[NI]) {
+    homog_keptN<T, NDC, NI>(P, Q, vis);
   }
   static __device__ __forceinline__ bool fast_ok(const T (&P)[IN], const Params&) { return homog_fast_ok<T>(P); }
   static __device__ __forceinline__ bool fast_try(const T (&P)[IN], const Params&, T (&Q)[OUT], bool& vis) {
@@ -388,6 +403,15 @@ template <typename T, class Op> __host__ __device__ constexpr bool compact_packe
 struct PackedKnobs {
   int warps, pw, nbuf, ilp;
 };
+#ifndef CLIPSEG_PK_COPYW
+#define CLIPSEG_PK_COPYW 0  // copy warps in the service warpgroup (0: compute warps copy their own batches)
+#endif
+#ifndef CLIPSEG_PK_REG_C
+#define CLIPSEG_PK_REG_C 112  // registers per compute thread with copy warps (setmaxnreg)
+#endif
+#ifndef CLIPSEG_PK_REG_S
+#define CLIPSEG_PK_REG_S 32   // registers per service thread with copy warps (512 x REG_C + 128 x REG_S <= 640 x 96: the CTA pool)
+#endif
 #ifndef CLIPSEG_PK_DEFER
 #define CLIPSEG_PK_DEFER 0  // 1: segments outside the fast path's range clipped in dense rounds of their own (C3 fp32 0.238 -> 0.211 ms at 1e7, but the headline 5.65 -> 6.18 ms and homogeneous 1.17 -> 1.77 ms: off)
 #endif
