@@ -1123,27 +1123,16 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
     int rank = 0;
     const uint32_t slix = INDEX ? sbase + (uint32_t)(S::kLixOff + ((size_t)b * W + warp) * BATCH) : 0u;
     int p0 = 0;
-    // Deferral (CLIPSEG_PK_DEFER): the first round holding a row outside the fast path's range
-    // switches the batch to deferred mode — from there on a fast row's result stays at its
-    // list position (visible bit in the bitmap) and an exceptional row's position is queued;
-    // the queue is then clipped by the rules in dense rounds and the rows from `dstart` on
-    // are compacted to their ranks.  Warps with a few exceptional rows thus run the fast
-    // path and the rules each on full rounds instead of both on every round.
-    constexpr bool DEFER = CLIPSEG_PK_DEFER != 0;
-    bool deferred = false;
-    int dstart = 0, nexc = 0;
-    // one row in deferred mode: the fast path, or the queue
-    auto defer_one = [&](int p, bool act, const T (&row)[IN], bool fok) -> bool {
-      T res[OUT];
-      bool vis = false, done = false;
-      if (fok) done = Op::fast_try(row, w, res, vis);
-      const bool q = act && !done;
-      const unsigned qm = __ballot_sync(0xFFFFFFFFu, q);
-      if (q) sts_u8(exc_a + nexc + __popc(qm & lt_mask), (uint32_t)p);
-      nexc += __popc(qm);
-      if (act && done) sts_row<T, OUT>(region + p * ROWB, res);
-      return act && done && vis;
-    };
+    // Exceptional rows (CLIPSEG_PK_DEFER): the main rounds run the fast path only; the first
+    // round holding a row outside its (cheap) range test ends them, and the batch's remaining
+    // rows [dstart, nkept) are finished in three passes — A: each row that passes the finer
+    // range test (Op::fast_ok2) is clipped by the fast path, its result left at its list
+    // position and its visible bit in the bitmap, the others are queued; B: the queue is
+    // clipped by the rules in dense rounds (results in place, bits OR-ed in); C: the rows are
+    // compacted to their ranks in order.  A warp thus never runs the rules on a round whose
+    // other lanes hold fast rows, and rows that only fail the cheap test (edge-touching WECs)
+    // stay on the fast path.  CLIPSEG_PK_DEFER 0: the per-lane fallback inside the rounds.
+    constexpr bool DEFER = S::K.defer;
     if constexpr (S::K.ilp >= 3) {  // NI rows per lane per round (this instantiation's knob)
       constexpr int NI = S::K.ilp;
       for (; nkept - p0 > 32 * (NI - 1); p0 += 32 * NI) {
@@ -1174,6 +1163,7 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
         }
       }
     }
+    bool brk = false;  // a main round met an exceptional row (DEFER)
     if constexpr (S::K.ilp >= 2) {  // (this instantiation's knob)
     for (; nkept - p0 > 32; p0 += 64) {
       const int pa = p0 + lane, pb = p0 + 32 + lane;
@@ -1185,28 +1175,22 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       const uint32_t ida = INDEX ? lds_u8(lidx_a + pa) : 0u, idb = INDEX ? lds_u8(lidx_a + pbr) : 0u;
       T qa[OUT], qb[OUT];
       bool va, vb;
-      if constexpr (DEFER) {
-        const bool fa = Op::fast_ok(ra, w), fb = Op::fast_ok(rb, w);
-        if (deferred || !__all_sync(0xFFFFFFFFu, fa & fb)) {
-          if (!deferred) {
-            deferred = true;
-            dstart = p0;
-          }
-          __syncwarp();
-          const bool wa = defer_one(pa, true, ra, fa), wb = defer_one(pb, actb, rb, fb);
-          const unsigned ma = __ballot_sync(0xFFFFFFFFu, wa), mb = __ballot_sync(0xFFFFFFFFu, wb);
-          if (lane == 0) {  // visible bits of the fast rows; the queued rows' bits are set later
-            sts_u32(vb_a + 4 * (p0 >> 5), ma);
-            sts_u32(vb_a + 4 * (p0 >> 5) + 4, mb);
-          }
-          continue;
-        }
-      }
 #ifdef CLIPSEG_ABL_NOMATH  // ablation builds only: the framework without the clip
       for (int c = 0; c < OUT; ++c) { qa[c] = ra[c]; qb[c] = rb[c]; }
       va = ra[0] < ra[2]; vb = rb[0] < rb[2];
 #else
-      Op::clip_two(ra, rb, w, qa, qb, va, vb);
+      if constexpr (DEFER) {
+        if (!__all_sync(0xFFFFFFFFu, Op::fast_ok(ra, w) & Op::fast_ok(rb, w))) {
+          brk = true;
+          break;
+        }
+        if (!__all_sync(0xFFFFFFFFu, Op::fast_two(ra, rb, w, qa, qb, va, vb))) {
+          brk = true;
+          break;
+        }
+      } else {
+        Op::clip_two(ra, rb, w, qa, qb, va, vb);
+      }
 #endif
       vb = vb & actb;
       __syncwarp();
@@ -1233,6 +1217,7 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       rank = rank_b + __popc(mb);
     }
     }
+    if (!brk) {
     for (; p0 < nkept; p0 += 32) {
       const int p = p0 + lane;
       const bool act = p < nkept;
@@ -1241,25 +1226,18 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       lds_row<T, IN>(region + pr * ROWB, row);
       const uint32_t id = INDEX ? lds_u8(lidx_a + pr) : 0u;
       T res[OUT];
-      if constexpr (DEFER) {
-        const bool fo = Op::fast_ok(row, w);
-        if (deferred || !__all_sync(0xFFFFFFFFu, fo)) {
-          if (!deferred) {
-            deferred = true;
-            dstart = p0;
-          }
-          __syncwarp();
-          const bool wv = defer_one(p, act, row, fo);
-          const unsigned m = __ballot_sync(0xFFFFFFFFu, wv);
-          if (lane == 0) sts_u32(vb_a + 4 * (p0 >> 5), m);
-          continue;
-        }
-      }
 #ifdef CLIPSEG_ABL_NOMATH
       for (int c = 0; c < OUT; ++c) res[c] = row[c];
       const bool vis = (row[0] < row[2]) & act;
 #else
-      const bool vis = Op::clip_one(row, w, res) & act;
+      bool vis;
+      if constexpr (DEFER) {
+        if (!__all_sync(0xFFFFFFFFu, Op::fast_ok(row, w))) break;
+        if (!__all_sync(0xFFFFFFFFu, Op::fast_try(row, w, res, vis))) break;
+        vis = vis & act;
+      } else {
+        vis = Op::clip_one(row, w, res) & act;
+      }
 #endif
       __syncwarp();
       if (early) copy_round();
@@ -1272,7 +1250,49 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       if (FLAGS && lane == 0) sts_u32(vb_a + 4 * (p0 >> 5), m);
       rank += __popc(m);
     }
-    if (DEFER && deferred) {
+    }
+    if (DEFER && p0 < nkept) {
+      const int dstart = p0;
+      int nexc = 0;
+      __syncwarp();
+      // pass A: the finer range test; fast rows clipped in place, the others queued.  Two rows
+      // per lane while more than 32 remain; the fast path runs on every row (a row that fails
+      // the test yields unused values), so the rounds are straight-line code.
+      auto pass_a = [&](int p, bool act, const T (&row)[IN], bool done, const T (&res)[OUT], bool vis) -> unsigned {
+        done = done && act && Op::fast_ok2(row, w);
+        const bool q = act && !done;
+        const unsigned qm = __ballot_sync(0xFFFFFFFFu, q);
+        if (q) sts_u8(exc_a + nexc + __popc(qm & lt_mask), (uint32_t)p);
+        nexc += __popc(qm);
+        if (done) sts_row<T, OUT>(region + p * ROWB, res);
+        return __ballot_sync(0xFFFFFFFFu, done && vis);
+      };
+      int q0 = dstart;
+      for (; nkept - q0 > 32; q0 += 64) {
+        const int pa = q0 + lane, pb = q0 + 32 + lane;
+        const bool actb = pb < nkept;
+        T ra[IN], rb[IN], qa[OUT], qb[OUT];
+        lds_row<T, IN>(region + pa * ROWB, ra);
+        lds_row<T, IN>(region + (actb ? pb : pa) * ROWB, rb);
+        bool va, vb;
+        const bool d = Op::fast_two(ra, rb, w, qa, qb, va, vb);
+        const unsigned ma = pass_a(pa, true, ra, d, qa, va);
+        const unsigned mb = pass_a(pb, actb, rb, d, qb, vb);
+        if (lane == 0) {
+          sts_u32(vb_a + 4 * (q0 >> 5), ma);
+          sts_u32(vb_a + 4 * (q0 >> 5) + 4, mb);
+        }
+      }
+      for (; q0 < nkept; q0 += 32) {
+        const int p = q0 + lane;
+        const bool act = p < nkept;
+        T row[IN], res[OUT];
+        lds_row<T, IN>(region + (act ? p : q0) * ROWB, row);
+        bool vis;
+        const bool d = Op::fast_try(row, w, res, vis);
+        const unsigned m = pass_a(p, act, row, d, res, vis);
+        if (lane == 0) sts_u32(vb_a + 4 * (q0 >> 5), m);
+      }
       __syncwarp();
       // pass B: the queued rows, by the rules, 32 per round (their results back in place)
       for (int e0 = 0; e0 < nexc; e0 += 32) {

@@ -31,13 +31,15 @@ template <typename T, int D> struct BoxOp : NoOutOfRange {  // axis-aligned clos
   // one segment R3 kept
   // R3 alone (bit v set: segment v kept); KeepParams are prepared once per launch
 #ifndef CLIPSEG_PK_KEEP
-#define CLIPSEG_PK_KEEP 0  // fp32 R3 test: 0 min/max compares (measured faster), 1 sign bits (FMA pipe + LOP3)
+#define CLIPSEG_PK_KEEP 2  // fp32 R3 test: 0 min/max compares and selects, 1 sign bits (FMA pipe + LOP3),
+                           // 2 min/max and one setp chain per segment (measured 5.65 -> 5.59 ms best at 1e9)
 #endif
   typedef KeepPrep<T, D> KeepParams;
   static __device__ __forceinline__ KeepParams keep_params(const Params& w) { return keep_prep<T, D>(w); }
   template <int V>
   static __device__ __forceinline__ unsigned keep(const T (&pl)[IN][V], const Params& w, const KeepParams& kp) {
     if constexpr (sizeof(T) == 4 && CLIPSEG_PK_KEEP == 1) return box_keep_sign<D, V>(pl, kp);
+    else if constexpr (sizeof(T) == 4 && CLIPSEG_PK_KEEP == 2) return box_keep_pred<D, V>(pl, w);
     else return box_keep<T, D, V>(pl, w);
   }
   static __device__ __forceinline__ bool clip_one(const T (&P)[IN], const Params& w, T (&Q)[OUT]) {
@@ -55,8 +57,15 @@ template <typename T, int D> struct BoxOp : NoOutOfRange {  // axis-aligned clos
   // deferred exceptional segments: the fast path's range test, the fast path alone (false:
   // the segment needs the rules) and the rules alone
   static __device__ __forceinline__ bool fast_ok(const T (&P)[IN], const Params& w) { return box_fast_ok<T, D>(P, w); }
+  static __device__ __forceinline__ bool fast_ok2(const T (&P)[IN], const Params& w) { return box_fast_ok2<T, D>(P, w); }
   static __device__ __forceinline__ bool fast_try(const T (&P)[IN], const Params& w, T (&Q)[OUT], bool& vis) {
     vis = clip_fast<T, D, false, true>(P, w, Q);
+    return true;
+  }
+  static __device__ __forceinline__ bool fast_two(const T (&Pa)[IN], const T (&Pb)[IN], const Params& w, T (&Qa)[OUT],
+                                                  T (&Qb)[OUT], bool& va, bool& vb) {
+    va = clip_fast<T, D, false, true>(Pa, w, Qa);
+    vb = clip_fast<T, D, false, true>(Pb, w, Qb);
     return true;
   }
   static __device__ __forceinline__ bool exact(const T (&P)[IN], const Params& w, T (&Q)[OUT]) {
@@ -123,6 +132,12 @@ struct IntOp {
     for (int i = 0; i < NI; ++i) vis[i] = clip_one(P[i], w, Q[i]);
   }
   static __device__ __forceinline__ bool fast_ok(const int32_t (&)[IN], const Params&) { return true; }
+  static __device__ __forceinline__ bool fast_ok2(const int32_t (&)[IN], const Params&) { return true; }
+  static __device__ __forceinline__ bool fast_two(const int32_t (&Pa)[IN], const int32_t (&Pb)[IN], const Params& w,
+                                                  int32_t (&Qa)[OUT], int32_t (&Qb)[OUT], bool& va, bool& vb) {
+    clip_two(Pa, Pb, w, Qa, Qb, va, vb);
+    return true;
+  }
   static __device__ __forceinline__ bool fast_try(const int32_t (&P)[IN], const Params& w, int32_t (&Q)[OUT], bool& vis) {
     vis = clip_one(P, w, Q);
     return true;
@@ -173,6 +188,19 @@ template <typename T, bool NDC> struct HomogOp : NoOutOfRange {  // NEXT-1: homo
     homog_keptN<T, NDC, NI>(P, Q, vis);
   }
   static __device__ __forceinline__ bool fast_ok(const T (&P)[IN], const Params&) { return homog_fast_ok<T>(P); }
+  static __device__ __forceinline__ bool fast_ok2(const T (&P)[IN], const Params&) { return homog_fast_ok<T>(P); }
+  static __device__ __forceinline__ bool fast_two(const T (&Pa)[IN], const T (&Pb)[IN], const Params&, T (&Qa)[OUT],
+                                                  T (&Qb)[OUT], bool& va, bool& vb) {
+    bool ok = true;
+    T qa[8], qb[8];
+    va = homog_fast<T, true>(Pa, qa, ok);
+    vb = homog_fast<T, true>(Pb, qb, ok);
+    if (ok) {
+      homog_emit<T, false, NDC>(qa, va, Qa);
+      homog_emit<T, false, NDC>(qb, vb, Qb);
+    }
+    return ok;
+  }
   static __device__ __forceinline__ bool fast_try(const T (&P)[IN], const Params&, T (&Q)[OUT], bool& vis) {
     bool ok = true;
     T q[8];
@@ -402,6 +430,7 @@ template <typename T, class Op> __host__ __device__ constexpr bool compact_packe
 // and fp64 (adversarial 0.72 -> 0.58 ms at 1e7).
 struct PackedKnobs {
   int warps, pw, nbuf, ilp;
+  bool defer;  // exceptional rows end the fast rounds and are finished in deferred passes
 };
 #ifndef CLIPSEG_PK_COPYW
 #define CLIPSEG_PK_COPYW 0  // copy warps in the service warpgroup (0: compute warps copy their own batches)
@@ -413,7 +442,13 @@ struct PackedKnobs {
 #define CLIPSEG_PK_REG_S 32   // registers per service thread with copy warps (512 x REG_C + 128 x REG_S <= 640 x 96: the CTA pool)
 #endif
 #ifndef CLIPSEG_PK_DEFER
-#define CLIPSEG_PK_DEFER 0  // 1: segments outside the fast path's range clipped in dense rounds of their own (C3 fp32 0.238 -> 0.211 ms at 1e7, but the headline 5.65 -> 6.18 ms and homogeneous 1.17 -> 1.77 ms: off)
+#define CLIPSEG_PK_DEFER 1  // deferred passes for 2D fp32 / fp64 (measured: C3 fp32 1e7 0.237 -> 0.155 ms,
+#endif                      // fp64 0.580 -> 0.523, headline unchanged)
+#ifndef CLIPSEG_PK3_DEFER
+#define CLIPSEG_PK3_DEFER 0  // 3D fp32: C4 0.876 -> 0.882 ms with deferral
+#endif
+#ifndef CLIPSEG_PKH_DEFER
+#define CLIPSEG_PKH_DEFER 0  // homogeneous fp32: 1.17 -> 1.49 ms with deferral (spills)
 #endif
 #ifndef CLIPSEG_PK3_ILP
 #define CLIPSEG_PK3_ILP 1
@@ -422,10 +457,12 @@ struct PackedKnobs {
 #define CLIPSEG_PKD_ILP 1
 #endif
 template <typename T, class Op> __host__ __device__ constexpr PackedKnobs packed_knobs() {
-  return Op::IN == 8          ? PackedKnobs{CLIPSEG_PKH_WARPS, 1, CLIPSEG_PKH_NBUF, CLIPSEG_PK_ILP}
-         : Op::IN == 6        ? PackedKnobs{CLIPSEG_PK3_WARPS, CLIPSEG_PK3_PW, CLIPSEG_PK3_NBUF, CLIPSEG_PK3_ILP}
-         : sizeof(T) == 8     ? PackedKnobs{CLIPSEG_PKD_WARPS, CLIPSEG_PKD_PW, 3, CLIPSEG_PKD_ILP}
-                              : PackedKnobs{CLIPSEG_PK_WARPS, CLIPSEG_PK_PW, CLIPSEG_PK_NBUF, CLIPSEG_PK_ILP};
+  return Op::IN == 8      ? PackedKnobs{CLIPSEG_PKH_WARPS, 1, CLIPSEG_PKH_NBUF, CLIPSEG_PK_ILP, CLIPSEG_PKH_DEFER != 0}
+         : Op::IN == 6    ? PackedKnobs{CLIPSEG_PK3_WARPS, CLIPSEG_PK3_PW, CLIPSEG_PK3_NBUF, CLIPSEG_PK3_ILP,
+                                     CLIPSEG_PK3_DEFER != 0}
+         : sizeof(T) == 8 ? PackedKnobs{CLIPSEG_PKD_WARPS, CLIPSEG_PKD_PW, 3, CLIPSEG_PKD_ILP, CLIPSEG_PK_DEFER != 0}
+                          : PackedKnobs{CLIPSEG_PK_WARPS, CLIPSEG_PK_PW, CLIPSEG_PK_NBUF, CLIPSEG_PK_ILP,
+                                        CLIPSEG_PK_DEFER != 0 && !std::is_same<Op, IntOp>::value};
 }
 template <typename T, class Op> __host__ __device__ constexpr int compact_min_blocks() {
   return compact_headline<T, Op>() ? CLIPSEG_MINB_F32_2D : 1;

@@ -17,6 +17,7 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=10**8)
+    ap.add_argument("--family", choices=["uniform", "adv"], default="uniform")
     a = ap.parse_args()
     import torch
     import synth
@@ -30,7 +31,8 @@ def main():
     L.clip_trace_clear.restype = ctypes.c_int
     n = a.n
     planes = clipseg.empty_planes(n, 2, torch.float32)
-    synth.fill_device(planes, synth.UNIFORM, 2, synth.seed_for(5), n)
+    fam = synth.UNIFORM if a.family == "uniform" else synth.ADVERSARIAL
+    synth.fill_device(planes, fam, 2, synth.seed_for(5), n)
     b = clipseg.CompactBuffers(n, 2, torch.float32, with_flags=True)
     w = clipseg.make_window([0, 0], [1, 1])
     s = torch.cuda.current_stream().cuda_stream
@@ -63,6 +65,15 @@ def main():
         "P_seen_to_copy_us": pct(tr[:, 6] - tr[:, 4]),
         "claim_order_vs_A_order_inversions": float(np.mean(np.diff(tr[:, 2]) < 0)),
     }
+    # per block: busy time (sum of start->A over its tiles) against the launch span
+    blk = t[ok][:, 7]
+    comp = (tr[:, 2] - tr[:, 1]).astype(np.float64)
+    busy = np.array([comp[blk == bb].sum() for bb in np.unique(blk)]) / 1000
+    ntl = np.array([(blk == bb).sum() for bb in np.unique(blk)])
+    res["block_busy_us"] = {p: round(float(np.percentile(busy, p)), 2) for p in (10, 50, 90)}
+    res["block_tiles"] = {p: int(np.percentile(ntl, p)) for p in (10, 50, 90)}
+    res["first_start_us"] = float(tr[:, 1].min()) / 1000
+    res["last_A_us"] = float(tr[:, 2].max()) / 1000
     # lateness of predecessor: A time of t-1 minus A time of t
     res["pred_A_later_than_mine_us"] = pct(np.maximum(tr[:-1, 2] - tr[1:, 2], 0))
     print(json.dumps(res, indent=1))
