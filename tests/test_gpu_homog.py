@@ -107,3 +107,38 @@ def test_large_sampled(torch, cs):
     n = 10**7
     planes = gen(n, 5, np.float32)
     check_compact(torch, cs, planes, n, True)
+
+
+@pytest.mark.parametrize("ndc", [False, True])
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_on_plane_grazing(torch, cs, ndc, dtype):
+    """P0 exactly on a clip plane (boundary coordinate +0: w0 = 1, x0 = -1 or +1) and P1 outside
+    that plane by a boundary coordinate of subnormal or tiny magnitude: the exiting alpha is
+    +0 / |b1|, the exact +0 — a fast path must not divide by a flushed subnormal.  Mixed into
+    the seeded HOMOG rows so every warp holds some."""
+    n = 20011
+    planes = gen(n, 7, dtype)
+    rng = np.random.default_rng(77)
+    emin = 149 if dtype == np.float32 else 1074
+    rows = np.nonzero(rng.random(n) < 0.2)[0]
+    for i in rows:
+        k = int(rng.integers(0, 3))
+        s = dtype(rng.choice([-1.0, 1.0]))  # the plane x_k = s w
+        planes[3, i] = dtype(1)
+        planes[k, i] = s
+        for c in range(3):
+            if c != k:
+                planes[c, i] = dtype(rng.uniform(-0.9, 0.9))
+        if rng.random() < 0.7:  # subnormal boundary coordinate of P1: w1 = 2^-(emin-22), |x1| = w1 + 2^-e
+            w1 = np.ldexp(dtype(1), -(emin - 22)).astype(dtype)
+            t = np.ldexp(dtype(1), -int(rng.integers(emin - 20, emin + 1))).astype(dtype)
+        else:  # tiny normal one
+            w1 = np.ldexp(dtype(1), -80).astype(dtype)
+            t = np.ldexp(dtype(1), -int(rng.integers(81, 100))).astype(dtype)
+        planes[7, i] = w1
+        planes[4 + k, i] = s * (w1 + t)  # boundary coordinate w1 - |x1| = -t exactly
+        for c in range(3):
+            if c != k:
+                planes[4 + c, i] = dtype(rng.uniform(-0.4, 0.4))
+    check_dense(torch, cs, planes, n, ndc)
+    check_compact(torch, cs, planes, n, ndc)
