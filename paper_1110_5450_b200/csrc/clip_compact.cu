@@ -794,6 +794,96 @@ __device__ __forceinline__ void lds_row(uint32_t a, T (&v)[N]) {
   }
 }
 
+// Staged rows of the packed kernel.  Rows of a multiple of 16 bytes are stored in 16-byte
+// slices: slice s of list row p sits at region + BATCH*16*s + 16*p, so a warp's accesses to
+// 32 consecutive rows are contiguous in every slice — 32-byte rows at their own stride put
+// twice the minimal wavefronts through the shared-memory banks (measured: homogeneous fp32
+// 1.186 -> 1.155 ms, fp64 2D 0.896 -> 0.881 ms at 1e8 / 5e7).  Rows of 16 bytes (2D fp32,
+// int32) are one slice, the plain array of rows; 24-byte rows (3D fp32) stay a plain array
+// (sliced as 16 + 8 bytes they measured 0.873 -> 0.877 ms).  The layout is fixed by the list
+// row's element count NIN; result rows (N <= NIN) use its slices.
+template <typename T, int NIN, int BATCH> struct RowSlices {
+  static constexpr int E = 16 / (int)sizeof(T);                // elements per slice
+  static constexpr int RB = NIN * (int)sizeof(T);              // row bytes
+  static constexpr bool PLAIN = RB % 16 != 0;                  // one slice: the array of rows
+  static constexpr int NS = PLAIN ? 1 : RB / 16;               // slices
+  static __host__ __device__ constexpr uint32_t stride(int) { return PLAIN ? (uint32_t)RB : 16u; }
+  static __host__ __device__ constexpr uint32_t off(int s) { return (uint32_t)BATCH * 16u * (uint32_t)s; }
+};
+template <typename T, int NIN, int BATCH, int N>
+__device__ __forceinline__ void sts_rowp(uint32_t region, int p, const T (&v)[N]) {
+  if constexpr (std::is_same<T, int32_t>::value) {
+    float f[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) f[i] = __int_as_float(v[i]);
+    sts_rowp<float, NIN, BATCH, N>(region, p, f);
+  } else if constexpr (RowSlices<T, NIN, BATCH>::PLAIN) {
+    sts_row<T, N>(region + (uint32_t)p * RowSlices<T, NIN, BATCH>::stride(0), v);
+  } else {
+    typedef RowSlices<T, NIN, BATCH> L;
+#pragma unroll
+    for (int sl = 0; sl < L::NS; ++sl) {
+      constexpr int E = L::E;
+      const int i0 = sl * E;
+      if (i0 < N) {
+        const uint32_t a = region + L::off(sl) + (uint32_t)p * L::stride(sl);
+        const int cnt = (N - i0 < E) ? N - i0 : E;
+        if (cnt * (int)sizeof(T) == 16) {
+          T x[E];
+#pragma unroll
+          for (int i = 0; i < E; ++i) x[i] = v[i0 + i < N ? i0 + i : i0];
+          sts_row<T, E>(a, x);
+        } else if constexpr (sizeof(T) == 4) {
+          if (cnt == 2) {
+            asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v[i0]), "f"(v[i0 + 1 < N ? i0 + 1 : i0]) : "memory");
+          } else {
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v[i0]) : "memory");
+          }
+        } else {
+          asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v[i0]) : "memory");
+        }
+      }
+    }
+  }
+}
+template <typename T, int NIN, int BATCH, int N>
+__device__ __forceinline__ void lds_rowp(uint32_t region, int p, T (&v)[N]) {
+  if constexpr (std::is_same<T, int32_t>::value) {
+    float f[N];
+    lds_rowp<float, NIN, BATCH, N>(region, p, f);
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = __float_as_int(f[i]);
+  } else if constexpr (RowSlices<T, NIN, BATCH>::PLAIN) {
+    lds_row<T, N>(region + (uint32_t)p * RowSlices<T, NIN, BATCH>::stride(0), v);
+  } else {
+    typedef RowSlices<T, NIN, BATCH> L;
+#pragma unroll
+    for (int sl = 0; sl < L::NS; ++sl) {
+      constexpr int E = L::E;
+      const int i0 = sl * E;
+      if (i0 < N) {
+        const uint32_t a = region + L::off(sl) + (uint32_t)p * L::stride(sl);
+        const int cnt = (N - i0 < E) ? N - i0 : E;
+        if (cnt * (int)sizeof(T) == 16) {
+          T x[E];
+          lds_row<T, E>(a, x);
+#pragma unroll
+          for (int i = 0; i < E; ++i)
+            if (i0 + i < N) v[i0 + i] = x[i];
+        } else if constexpr (sizeof(T) == 4) {
+          if (cnt == 2) {
+            asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v[i0]), "=f"(v[i0 + 1 < N ? i0 + 1 : i0]) : "r"(a) : "memory");
+          } else {
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[i0]) : "r"(a) : "memory");
+          }
+        } else {
+          asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v[i0]) : "r"(a) : "memory");
+        }
+      }
+    }
+  }
+}
+
 #ifndef CLIPSEG_PK_SCANPUB
 #define CLIPSEG_PK_SCANPUB 0  // 1: the scan warp publishes each aggregate (measured 5.73 -> 11.1 ms: it then waits for its
                               // prefix before publishing the next tile, serialising the blocks)
@@ -814,7 +904,6 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
   typedef PackedShape<T, Op, INDEX> S;
   constexpr int IN = S::IN, OUT = S::OUT, V = S::V, SUB = S::SUB, PW = S::PW, BATCH = S::BATCH, W = S::W;
   constexpr int BT = S::BT, NBUF = S::NBUF;
-  constexpr uint32_t ROWB = (uint32_t)S::ROWB;  // staged row bytes (list rows and output rows)
   static_assert(NBUF >= 2 && NBUF <= kTileRing - 3, "tile ring");
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -892,7 +981,7 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
         for (int w2 = cw; w2 < W; w2 += CW) {
           const int cnt = s_cnt[bb][w2];
           const int64_t g0 = prefix + s_pre[bb][w2];
-          const uint32_t reg = sb + (uint32_t)(((size_t)bb * W + w2) * S::kRegion * sizeof(T)) + lane * ROWB;
+          const uint32_t reg = sb + (uint32_t)(((size_t)bb * W + w2) * S::kRegion * sizeof(T));
           T* dst[OUT];
 #pragma unroll
           for (int c = 0; c < OUT; ++c) dst[c] = out + c * ld_out + g0 + lane;
@@ -902,8 +991,8 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
           for (int q = 0; q < BATCH / 32; ++q) {
             if (q * 32 >= cnt) break;
             if (q * 32 + lane < cnt) {
-              T row[IN];
-              lds_row<T, IN>(reg + q * 32 * ROWB, row);
+              T row[OUT];
+              lds_rowp<T, IN, BATCH>(reg, q * 32 + lane, row);
 #pragma unroll
               for (int c = 0; c < OUT; ++c) __stcs(dst[c] + q * 32, row[c]);
               if (INDEX) out_index[g0 + q * 32 + lane] = ib + lds_u8(slix + q * 32);
@@ -969,7 +1058,7 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
     if (warp == 0 && lane == 0) CLIP_TRACE(tk, 6, trace_now());
     const int cnt = s_cnt[cb][warp];
     const int64_t g0 = s_prefix[cb] + s_pre[cb][warp];
-    const uint32_t reg = region_of(cb) + lane * ROWB;
+    const uint32_t creg0 = region_of(cb);
     T* dst[OUT];  // per-plane row pointers, computed once per batch
 #pragma unroll
     for (int c = 0; c < OUT; ++c) dst[c] = out + c * ld_out + g0 + lane;
@@ -982,10 +1071,10 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
 #pragma unroll
     for (int q0 = 0; q0 < BATCH / 32; q0 += CH) {
       if (q0 * 32 >= cnt) break;
-      T rows[CH][IN];
+      T rows[CH][OUT];
 #pragma unroll
       for (int u = 0; u < CH; ++u)
-        if ((q0 + u) * 32 + lane < cnt) lds_row<T, IN>(reg + (q0 + u) * 32 * ROWB, rows[u]);
+        if ((q0 + u) * 32 + lane < cnt) lds_rowp<T, IN, BATCH>(creg0, (q0 + u) * 32 + lane, rows[u]);
 #pragma unroll
       for (int u = 0; u < CH; ++u) {
         const int q = q0 + u;
@@ -1072,7 +1161,7 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
           T row[IN];
 #pragma unroll
           for (int c = 0; c < IN; ++c) row[c] = cur[j][c][v];
-          sts_row<T, IN>(region + pos * ROWB, row);
+          sts_rowp<T, IN, BATCH>(region, pos, row);
           if (INDEX) sts_u8(lidx_a + pos, (uint32_t)(j * SUB + lane * V + v));
         }
         pos += kv;
@@ -1101,7 +1190,7 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       early = true;
       cpar ^= 1u << cb;
       ccnt = s_cnt[cb][warp];
-      creg = region_of(cb) + lane * ROWB;
+      creg = region_of(cb);
       const int64_t g0 = s_prefix[cb] + s_pre[cb][warp];
 #pragma unroll
       for (int c = 0; c < OUT; ++c) cdst[c] = out + c * ld_out + g0 + lane;
@@ -1109,8 +1198,8 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
     auto copy_round = [&]() {  // warp-uniform: one 32-row round of the early copy-out
       if (cq * 32 < ccnt) {
         if (cq * 32 + lane < ccnt) {
-          T row[IN];
-          lds_row<T, IN>(creg + cq * 32 * ROWB, row);
+          T row[OUT];
+          lds_rowp<T, IN, BATCH>(creg, cq * 32 + lane, row);
 #pragma unroll
           for (int c = 0; c < OUT; ++c) __stcs(cdst[c] + cq * 32, row[c]);
         }
@@ -1144,7 +1233,7 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
           const int p = p0 + 32 * i + lane;
           ac[i] = p < nkept;
           const int pr = ac[i] ? p : p0 + lane;  // an idle row re-clips the round's first one
-          lds_row<T, IN>(region + pr * ROWB, rr[i]);
+          lds_rowp<T, IN, BATCH>(region, pr, rr[i]);
           id[i] = INDEX ? lds_u8(lidx_a + pr) : 0u;
         }
         Op::template clip_n<NI>(rr, w, qq, vv);
@@ -1155,7 +1244,7 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
           const unsigned m = __ballot_sync(0xFFFFFFFFu, v);
           if (v) {
             const int r = rank + __popc(m & lt_mask);
-            sts_row<T, OUT>(region + r * ROWB, qq[i]);
+            sts_rowp<T, IN, BATCH>(region, r, qq[i]);
             if (INDEX) sts_u8(slix + r, id[i]);
           }
           if (FLAGS && lane == 0) sts_u32(vb_a + 4 * ((p0 >> 5) + i), m);
@@ -1170,8 +1259,8 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       const bool actb = pb < nkept;
       const int pbr = actb ? pb : pa;  // an idle second item re-clips the first (same path, no divergence)
       T ra[IN], rb[IN];
-      lds_row<T, IN>(region + pa * ROWB, ra);
-      lds_row<T, IN>(region + pbr * ROWB, rb);
+      lds_rowp<T, IN, BATCH>(region, pa, ra);
+      lds_rowp<T, IN, BATCH>(region, pbr, rb);
       const uint32_t ida = INDEX ? lds_u8(lidx_a + pa) : 0u, idb = INDEX ? lds_u8(lidx_a + pbr) : 0u;
       T qa[OUT], qb[OUT];
       bool va, vb;
@@ -1202,12 +1291,12 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       const int rank_b = rank + __popc(ma);
       if (va) {
         const int r = rank + __popc(ma & lt_mask);
-        sts_row<T, OUT>(region + r * ROWB, qa);
+        sts_rowp<T, IN, BATCH>(region, r, qa);
         if (INDEX) sts_u8(slix + r, ida);
       }
       if (vb) {
         const int r = rank_b + __popc(mb & lt_mask);
-        sts_row<T, OUT>(region + r * ROWB, qb);
+        sts_rowp<T, IN, BATCH>(region, r, qb);
         if (INDEX) sts_u8(slix + r, idb);
       }
       if (FLAGS && lane == 0) {
@@ -1223,7 +1312,7 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       const bool act = p < nkept;
       const int pr = act ? p : p0;  // an idle lane re-clips the round's first row
       T row[IN];
-      lds_row<T, IN>(region + pr * ROWB, row);
+      lds_rowp<T, IN, BATCH>(region, pr, row);
       const uint32_t id = INDEX ? lds_u8(lidx_a + pr) : 0u;
       T res[OUT];
 #ifdef CLIPSEG_ABL_NOMATH
@@ -1244,7 +1333,7 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       const unsigned m = __ballot_sync(0xFFFFFFFFu, vis);
       if (vis) {
         const int r = rank + __popc(m & lt_mask);
-        sts_row<T, OUT>(region + r * ROWB, res);
+        sts_rowp<T, IN, BATCH>(region, r, res);
         if (INDEX) sts_u8(slix + r, id);
       }
       if (FLAGS && lane == 0) sts_u32(vb_a + 4 * (p0 >> 5), m);
@@ -1264,7 +1353,7 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
         const unsigned qm = __ballot_sync(0xFFFFFFFFu, q);
         if (q) sts_u8(exc_a + nexc + __popc(qm & lt_mask), (uint32_t)p);
         nexc += __popc(qm);
-        if (done) sts_row<T, OUT>(region + p * ROWB, res);
+        if (done) sts_rowp<T, IN, BATCH>(region, p, res);
         return __ballot_sync(0xFFFFFFFFu, done && vis);
       };
       int q0 = dstart;
@@ -1272,8 +1361,8 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
         const int pa = q0 + lane, pb = q0 + 32 + lane;
         const bool actb = pb < nkept;
         T ra[IN], rb[IN], qa[OUT], qb[OUT];
-        lds_row<T, IN>(region + pa * ROWB, ra);
-        lds_row<T, IN>(region + (actb ? pb : pa) * ROWB, rb);
+        lds_rowp<T, IN, BATCH>(region, pa, ra);
+        lds_rowp<T, IN, BATCH>(region, (actb ? pb : pa), rb);
         bool va, vb;
         const bool d = Op::fast_two(ra, rb, w, qa, qb, va, vb);
         const unsigned ma = pass_a(pa, true, ra, d, qa, va);
@@ -1287,7 +1376,7 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
         const int p = q0 + lane;
         const bool act = p < nkept;
         T row[IN], res[OUT];
-        lds_row<T, IN>(region + (act ? p : q0) * ROWB, row);
+        lds_rowp<T, IN, BATCH>(region, (act ? p : q0), row);
         bool vis;
         const bool d = Op::fast_try(row, w, res, vis);
         const unsigned m = pass_a(p, act, row, d, res, vis);
@@ -1300,10 +1389,10 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
         const bool act = e < nexc;
         const int p = (int)lds_u8(exc_a + (act ? e : e0));
         T row[IN], res[OUT];
-        lds_row<T, IN>(region + p * ROWB, row);
+        lds_rowp<T, IN, BATCH>(region, p, row);
         const bool vis = Op::exact(row, w, res);
         if (act) {
-          sts_row<T, OUT>(region + p * ROWB, res);
+          sts_rowp<T, IN, BATCH>(region, p, res);
           if (vis) atom_or_shared_a(vb_a + 4 * (p >> 5), 1u << (p & 31));
         }
       }
@@ -1313,14 +1402,14 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
         const int p = q0 + lane;
         const bool act = p < nkept;
         T row[OUT];  // results (OUT elements) sit at the rows' list positions
-        if (act) lds_row<T, OUT>(region + p * ROWB, row);
+        if (act) lds_rowp<T, IN, BATCH>(region, p, row);
         const bool vis = act && ((lds_u32(vb_a + 4 * (q0 >> 5)) >> lane) & 1u);
         const uint32_t id = (INDEX && act) ? lds_u8(lidx_a + p) : 0u;
         __syncwarp();
         const unsigned m = __ballot_sync(0xFFFFFFFFu, vis);
         if (vis) {
           const int r = rank + __popc(m & lt_mask);
-          sts_row<T, OUT>(region + r * ROWB, row);
+          sts_rowp<T, IN, BATCH>(region, r, row);
           if (INDEX) sts_u8(slix + r, id);
         }
         rank += __popc(m);

@@ -383,26 +383,36 @@ template <typename T, class Op> __host__ __device__ constexpr bool compact_prefe
 #ifndef CLIPSEG_PK_NBUF
 #define CLIPSEG_PK_NBUF 3
 #endif
-// fp32 3D cuboid (C4): rows of 24 B, so one sub-tile per warp batch keeps the register
-// prefetch (24 floats) and the staging (15 warps x 3 x 3 KB) within budget.
+// fp32 3D cuboid (C4): rows of 24 B; 10 compute warps with two sub-tiles (256 segments) per
+// batch (staging 10 warps x 3 x 6 KB, 156 registers for the 48-float prefetch) measured
+// 0.875 -> 0.832 ms at 1e8 against 15 warps x 128 segments (9 / 11 / 12 warps x 256: 0.93 /
+// 0.887 / 0.894; two rows per lane: 0.8325).
 #ifndef CLIPSEG_PACKED_F32_3D
 #define CLIPSEG_PACKED_F32_3D 1
 #endif
 #ifndef CLIPSEG_PK3_WARPS
-#define CLIPSEG_PK3_WARPS 15
+#define CLIPSEG_PK3_WARPS 10
 #endif
 #ifndef CLIPSEG_PK3_PW
-#define CLIPSEG_PK3_PW 1
+#define CLIPSEG_PK3_PW 2
 #endif
 #ifndef CLIPSEG_PK3_NBUF
 #define CLIPSEG_PK3_NBUF 3
 #endif
-// fp32 homogeneous (NEXT-1): rows of 32 B, one sub-tile per warp batch.
+// fp32 homogeneous (NEXT-1): rows of 32 B, one sub-tile per warp batch (6 / 7 / 8 warps with
+// two sub-tiles measured 1.43 / 1.25 / 1.33 ms against 1.15 at 1e8; 13 / 14 warps x 128:
+// 1.30 / 1.23).
 #ifndef CLIPSEG_PACKED_F32_H
 #define CLIPSEG_PACKED_F32_H 1
 #endif
 #ifndef CLIPSEG_PKH_WARPS
 #define CLIPSEG_PKH_WARPS 15
+#endif
+#ifndef CLIPSEG_PKH_PW
+#define CLIPSEG_PKH_PW 1
+#endif
+#ifndef CLIPSEG_PKH_ILP
+#define CLIPSEG_PKH_ILP CLIPSEG_PK_ILP
 #endif
 #ifndef CLIPSEG_PKH_NBUF
 #define CLIPSEG_PKH_NBUF 3
@@ -457,7 +467,7 @@ struct PackedKnobs {
 #define CLIPSEG_PKD_ILP 1
 #endif
 template <typename T, class Op> __host__ __device__ constexpr PackedKnobs packed_knobs() {
-  return Op::IN == 8      ? PackedKnobs{CLIPSEG_PKH_WARPS, 1, CLIPSEG_PKH_NBUF, CLIPSEG_PK_ILP, CLIPSEG_PKH_DEFER != 0}
+  return Op::IN == 8      ? PackedKnobs{CLIPSEG_PKH_WARPS, CLIPSEG_PKH_PW, CLIPSEG_PKH_NBUF, CLIPSEG_PKH_ILP, CLIPSEG_PKH_DEFER != 0}
          : Op::IN == 6    ? PackedKnobs{CLIPSEG_PK3_WARPS, CLIPSEG_PK3_PW, CLIPSEG_PK3_NBUF, CLIPSEG_PK3_ILP,
                                      CLIPSEG_PK3_DEFER != 0}
          : sizeof(T) == 8 ? PackedKnobs{CLIPSEG_PKD_WARPS, CLIPSEG_PKD_PW, 3, CLIPSEG_PKD_ILP, CLIPSEG_PK_DEFER != 0}

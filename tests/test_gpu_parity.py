@@ -13,9 +13,11 @@ import synth
 pytestmark = pytest.mark.gpu
 
 UNIT = {2: ([0.0, 0.0], [1.0, 1.0]), 3: ([0.0, 0.0, 0.0], [1.0, 1.0, 1.0])}
-# sizes spanning several compacting tiles (fp32 2D 4096, fp32 3D 2816, fp64 2D 2048, fp64 3D
-# 1024 segments) with exact and ragged ends
+# sizes spanning several compacting tiles with exact and ragged ends (round-1 tiles: fp32 2D
+# 4096, fp32 3D 2816, fp64 2D 2048, fp64 3D 1024 segments; packed-kernel tiles: PACKED_TILES)
 SIZES = [1, 3, 4, 5, 31, 1023, 1024, 1025, 2815, 2816, 2817, 4097, 8448, 10007, 100003, 1 << 20]
+# packed compacting kernel block tiles (compute warps x batch, clip_kernels.cuh knobs)
+PACKED_TILES = {(2, np.float32): 15 * 256, (3, np.float32): 10 * 256, (2, np.float64): 11 * 128}
 
 
 @pytest.fixture(scope="module")
@@ -126,6 +128,22 @@ def test_dense_in_place(torch, cs):
 def test_compact_2d_f32_sizes(torch, cs, n):
     planes, _ = gen(synth.UNIFORM, 2, synth.seed_for(5), n, np.float32)
     check_compact(torch, cs, planes, n, *UNIT[2], 2, index_base=12345)
+
+
+@pytest.mark.parametrize("key", list(PACKED_TILES))
+@pytest.mark.parametrize("m", [(1, -1), (1, 0), (1, 1), (2, 1), (3, -1), (7, 13)])
+def test_compact_packed_tile_edges(torch, cs, key, m):
+    dim, dtype = key
+    n = m[0] * PACKED_TILES[key] + m[1]
+    planes, _ = gen(synth.ADVERSARIAL if m[0] == 7 else synth.UNIFORM, dim, synth.seed_for(5, n), n, dtype)
+    check_compact(torch, cs, planes, n, *UNIT[dim], dim, index_base=777)
+    # the bench's instantiation: flags, no index
+    want, _, wcnt, wflags = oracle.compact(planes, n, *UNIT[dim], dim, with_flags=True)
+    b = cs.clip_compact(to_dev(torch, planes), n, *UNIT[dim], with_flags=True)
+    torch.cuda.synchronize()
+    assert int(b.count.item()) == wcnt
+    assert np.array_equal(b.flags.cpu().numpy()[:n], wflags)
+    assert np.array_equal(bits(b.out.cpu().numpy()[:, :wcnt]), bits(want[:, :wcnt]))
 
 
 @pytest.mark.parametrize("dim", [2, 3])
