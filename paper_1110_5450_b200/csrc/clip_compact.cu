@@ -293,6 +293,101 @@ __device__ __forceinline__ void tile_scan_warp(int lane, int64_t ntiles, unsigne
   }
 }
 
+// Block 0's scan warp in the packed kernel: the global scanner above, interleaved with the
+// tile duties of tile_scan_warp for block 0's own tiles, both non-blocking (mbarrier tests
+// instead of waits), so block 0 computes tiles too instead of leaving one SM idle.  Its own
+// tile's inclusive prefix is read back once the scanner's frontier has passed the tile.
+template <int NSUB, int NBUF>
+__device__ __forceinline__ void scanner_with_tiles(int lane, int64_t ntiles, unsigned long long* status,
+                                                   int64_t* d_count, const int64_t* s_tile, const int (*s_cnt)[NSUB],
+                                                   int (*s_pre)[NSUB], int64_t* s_prefix, int* s_done,
+                                                   uint64_t* mb_tile, uint64_t* mb_cnt, uint64_t* mb_pre) {
+  static_assert(NSUB <= 64, "two counts per lane");
+  constexpr int M = kScanPerLane;
+  int64_t base = 0;
+  unsigned long long running = 0;
+  int64_t k = 0, tile = 0, total = 0;
+  int b = 0, state = 0;  // tile duty of iteration k: 0 claim, 1 counts, 2 prefix, 3 no tiles left
+  unsigned par = 0;      // bit q: parity of the next phase of mb_cnt[q] / mb_pre[q]
+  while (base < ntiles || state != 3) {
+    if (base < ntiles) {  // ---- one scanner probe
+      unsigned long long sv[M];
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        const int64_t idx = base + lane * M + j;
+        sv[j] = (idx < ntiles) ? ld_relaxed(status + idx) : 0ull;
+      }
+      int myx = M;
+#pragma unroll
+      for (int j = M - 1; j >= 0; --j)
+        if ((sv[j] >> 62) == 0u) myx = j;
+      const unsigned xmask = __ballot_sync(0xFFFFFFFFu, myx < M);
+      const int fl = xmask ? __ffs(xmask) - 1 : 32;
+      const int ready = (fl == 32) ? 32 * M : fl * M + __shfl_sync(0xFFFFFFFFu, myx, fl & 31);
+      if (ready > 0) {
+        unsigned long long vsum = 0;
+#pragma unroll
+        for (int j = 0; j < M; ++j)
+          if (lane * M + j < ready) vsum += sv[j] & kValueMask;
+        unsigned long long incl = vsum;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const unsigned long long y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+          if (lane >= d) incl += y;
+        }
+        unsigned long long run = running + incl - vsum;
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+          if (lane * M + j < ready) {
+            run += sv[j] & kValueMask;
+            st_relaxed(status + base + lane * M + j, kFlagP | run);
+            CLIP_TRACE(base + lane * M + j, 5, trace_now());
+          }
+        }
+        running += __shfl_sync(0xFFFFFFFFu, incl, 31);
+        base += ready;
+        __syncwarp();  // the published prefixes are visible to lane 0's read-back below
+      }
+    }
+    // ---- block 0's own tile of iteration k
+    if (state == 0 && mbar_test_a(smem_addr(&mb_tile[k & kRingMask]), (uint32_t)((k / kTileRing) & 1))) {
+      tile = s_tile[k & kRingMask];
+      state = tile >= ntiles ? 3 : 1;
+    }
+    if (state == 1 && mbar_test_a(smem_addr(&mb_cnt[b]), (par >> b) & 1u)) {
+      const int c0 = (lane < NSUB) ? s_cnt[b][lane] : 0;
+      const int c1 = (NSUB > 32 && lane + 32 < NSUB) ? s_cnt[b][lane + 32] : 0;
+      const int c = c0 | (c1 << 16);
+      int incl = c;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+        if (lane >= d) incl += y;
+      }
+      const int tot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      if (lane < NSUB) s_pre[b][lane] = (incl & 0xFFFF) - c0;
+      if (NSUB > 32 && lane + 32 < NSUB) s_pre[b][lane + 32] = (tot & 0xFFFF) + (incl >> 16) - c1;
+      total = (tot & 0xFFFF) + (tot >> 16);
+      state = 2;
+    }
+    if (state == 2 && tile < base) {  // the scanner has published the tile's inclusive prefix
+      if (lane == 0) {
+        const unsigned long long st = ld_relaxed(status + tile);
+        st_relaxed(status + tile, 0ull);  // consumed: leave the word clean for the next call
+        s_prefix[b] = (int64_t)(st & kValueMask) - total;
+        s_done[b] = 0;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&mb_pre[b]);
+      par ^= 1u << b;
+      b = (b + 1 == NBUF) ? 0 : b + 1;
+      ++k;
+      state = 0;
+    }
+  }
+  if (lane == 0) *d_count = (int64_t)running;
+}
+
 // Workspace header: [0] tile-claim counter, [1] finished-block counter.  The last block of
 // the grid to finish resets both, so (with the status words zeroed by the scan warps) the
 // workspace is all zero after every launch.  Called by one warp per block, after every other
@@ -942,7 +1037,7 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
     for (int q = 0; q < kTileRing; ++q) mbar_init(&mb_tile[q], 1);
     if (CW)
       for (int q = 0; q < NBUF; ++q) mbar_init(&mb_free[q], CW);
-    if (blockIdx.x != 0) {  // the tiles of iterations 0 and 1
+    if (S::K.b0tiles || blockIdx.x != 0) {  // the tiles of iterations 0 and 1
       s_tile[0] = (int64_t)atom_add_global(counter, 1ull);
       s_tile[1] = (int64_t)atom_add_global(counter, 1ull);
       mbar_arrive(&mb_tile[0]);
@@ -950,7 +1045,7 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
     }
   }
   __syncthreads();
-  if (blockIdx.x == 0) {
+  if (!S::K.b0tiles && blockIdx.x == 0) {
     if (warp == W) {
       global_scanner(status, ntiles, lane, d_count);
       block_exit(ws, lane);
@@ -961,8 +1056,12 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
     // warpgroup register split: the service warps give registers to the compute warps
     if constexpr (CW > 0) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(CLIPSEG_PK_REG_S));
     if (warp == W) {
-      tile_scan_warp<W, NBUF>(lane, ntiles, status, s_tile, s_cnt, s_pre, s_prefix, s_done, mb_tile, mb_cnt, mb_pre,
-                              nullptr, CLIPSEG_PK_SCANPUB != 0);
+      if (S::K.b0tiles && blockIdx.x == 0)
+        scanner_with_tiles<W, NBUF>(lane, ntiles, status, d_count, s_tile, s_cnt, s_pre, s_prefix, s_done, mb_tile,
+                                    mb_cnt, mb_pre);
+      else
+        tile_scan_warp<W, NBUF>(lane, ntiles, status, s_tile, s_cnt, s_pre, s_prefix, s_done, mb_tile, mb_cnt,
+                                mb_pre, nullptr, CLIPSEG_PK_SCANPUB != 0);
       block_exit(ws, lane);
       return;
     }
@@ -1492,7 +1591,8 @@ static cudaError_t launch_packed_variant(const T* in, int64_t ld_in, int64_t n, 
   cudaError_t e = kernel_occupancy((const void*)kern, S::kThreads, S::kSmemBytes, &blocks_per_sm);
   if (e != cudaSuccess) return e;
   const int64_t cap = (int64_t)device_sm_count() * blocks_per_sm;
-  const int grid = (int)(ntiles + 1 < cap ? ntiles + 1 : cap);
+  const int64_t want = S::K.b0tiles ? (ntiles > 1 ? ntiles : 1) : ntiles + 1;  // (block 0 computes too)
+  const int grid = (int)(want < cap ? want : cap);
   void* args[] = {(void*)&in,     (void*)&ld_in,     (void*)&n,          (void*)&w,     (void*)&out,
                   (void*)&ld_out, (void*)&out_index, (void*)&index_base, (void*)&flags, (void*)&d_count,
                   (void*)&ws,     (void*)&ntiles};

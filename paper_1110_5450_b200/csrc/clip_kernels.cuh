@@ -440,8 +440,19 @@ template <typename T, class Op> __host__ __device__ constexpr bool compact_packe
 // and fp64 (adversarial 0.72 -> 0.58 ms at 1e7).
 struct PackedKnobs {
   int warps, pw, nbuf, ilp;
-  bool defer;  // exceptional rows end the fast rounds and are finished in deferred passes
+  bool defer;    // exceptional rows end the fast rounds and are finished in deferred passes
+  bool b0tiles;  // block 0 processes tiles too, its scan warp interleaving the global scanner
 };
+// Block 0 taking tiles (its scan warp runs the global scanner and its own tile duties,
+// non-blocking): measured 3D 0.834 -> 0.829 ms at 1e8 and C3 fp32 0.149 -> 0.147 ms, but the
+// headline 5.586 -> 5.624 ms best at 1e9 — the scanner, on whose latency every copy-out
+// waits, then shares its SM with 15 compute warps.  On for 3D only.
+#ifndef CLIPSEG_PK_B0TILES
+#define CLIPSEG_PK_B0TILES 0
+#endif
+#ifndef CLIPSEG_PK3_B0TILES
+#define CLIPSEG_PK3_B0TILES 1
+#endif
 #ifndef CLIPSEG_PK_COPYW
 #define CLIPSEG_PK_COPYW 0  // copy warps in the service warpgroup (0: compute warps copy their own batches)
 #endif
@@ -467,12 +478,15 @@ struct PackedKnobs {
 #define CLIPSEG_PKD_ILP 1
 #endif
 template <typename T, class Op> __host__ __device__ constexpr PackedKnobs packed_knobs() {
-  return Op::IN == 8      ? PackedKnobs{CLIPSEG_PKH_WARPS, CLIPSEG_PKH_PW, CLIPSEG_PKH_NBUF, CLIPSEG_PKH_ILP, CLIPSEG_PKH_DEFER != 0}
+  return Op::IN == 8      ? PackedKnobs{CLIPSEG_PKH_WARPS, CLIPSEG_PKH_PW, CLIPSEG_PKH_NBUF, CLIPSEG_PKH_ILP,
+                                     CLIPSEG_PKH_DEFER != 0, CLIPSEG_PK_B0TILES != 0}
          : Op::IN == 6    ? PackedKnobs{CLIPSEG_PK3_WARPS, CLIPSEG_PK3_PW, CLIPSEG_PK3_NBUF, CLIPSEG_PK3_ILP,
-                                     CLIPSEG_PK3_DEFER != 0}
-         : sizeof(T) == 8 ? PackedKnobs{CLIPSEG_PKD_WARPS, CLIPSEG_PKD_PW, 3, CLIPSEG_PKD_ILP, CLIPSEG_PK_DEFER != 0}
+                                     CLIPSEG_PK3_DEFER != 0, CLIPSEG_PK3_B0TILES != 0}
+         : sizeof(T) == 8 ? PackedKnobs{CLIPSEG_PKD_WARPS, CLIPSEG_PKD_PW, 3, CLIPSEG_PKD_ILP, CLIPSEG_PK_DEFER != 0,
+                                        CLIPSEG_PK_B0TILES != 0}
                           : PackedKnobs{CLIPSEG_PK_WARPS, CLIPSEG_PK_PW, CLIPSEG_PK_NBUF, CLIPSEG_PK_ILP,
-                                        CLIPSEG_PK_DEFER != 0 && !std::is_same<Op, IntOp>::value};
+                                        CLIPSEG_PK_DEFER != 0 && !std::is_same<Op, IntOp>::value,
+                                        CLIPSEG_PK_B0TILES != 0};
 }
 template <typename T, class Op> __host__ __device__ constexpr int compact_min_blocks() {
   return compact_headline<T, Op>() ? CLIPSEG_MINB_F32_2D : 1;
