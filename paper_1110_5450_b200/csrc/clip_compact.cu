@@ -1130,10 +1130,24 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
     return r >= BATCH ? BATCH : (r > 0 ? (int)r : 0);
   };
   T cur[PW][IN][V];
+#ifndef CLIPSEG_PK_PLANEPTR
+#define CLIPSEG_PK_PLANEPTR 0  // 1: per-plane base pointers held across the loop (fewer 64-bit address ops per load)
+#endif
+  const T* plane_in[CLIPSEG_PK_PLANEPTR ? IN : 1];
+#pragma unroll
+  for (int c = 0; c < (CLIPSEG_PK_PLANEPTR ? IN : 1); ++c) plane_in[c] = lane_in + c * ld_in;
   auto load = [&](int64_t t) {
     const T* src = lane_in + t * BT;
     const int rem = batch_rem(t);
-    if (rem == BATCH) {  // warp-uniform: full batch, unpredicated loads
+    if (CLIPSEG_PK_PLANEPTR && rem == BATCH) {
+      const int64_t off = t * BT;
+#pragma unroll
+      for (int c = 0; c < IN; ++c) {
+        const T* sc = plane_in[CLIPSEG_PK_PLANEPTR ? c : 0] + off;
+#pragma unroll
+        for (int j = 0; j < PW; ++j) load_vec<T, IN == 4>(sc + j * SUB, cur[j][c]);
+      }
+    } else if (rem == BATCH) {  // warp-uniform: full batch, unpredicated loads
 #pragma unroll
       for (int c = 0; c < IN; ++c) {
         const T* sc = src + c * ld_in;
@@ -1372,7 +1386,9 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
           brk = true;
           break;
         }
-        if (!__all_sync(0xFFFFFFFFu, Op::fast_two(ra, rb, w, qa, qb, va, vb))) {
+        if constexpr (Op::kFastAlwaysDone) {  // (no warp vote on a constant)
+          Op::fast_two(ra, rb, w, qa, qb, va, vb);
+        } else if (!__all_sync(0xFFFFFFFFu, Op::fast_two(ra, rb, w, qa, qb, va, vb))) {
           brk = true;
           break;
         }
@@ -1421,7 +1437,11 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       bool vis;
       if constexpr (DEFER) {
         if (!__all_sync(0xFFFFFFFFu, Op::fast_ok(row, w))) break;
-        if (!__all_sync(0xFFFFFFFFu, Op::fast_try(row, w, res, vis))) break;
+        if constexpr (Op::kFastAlwaysDone) {
+          Op::fast_try(row, w, res, vis);
+        } else if (!__all_sync(0xFFFFFFFFu, Op::fast_try(row, w, res, vis))) {
+          break;
+        }
         vis = vis & act;
       } else {
         vis = Op::clip_one(row, w, res) & act;

@@ -56,6 +56,7 @@ template <typename T, int D> struct BoxOp : NoOutOfRange {  // axis-aligned clos
   }
   // deferred exceptional segments: the fast path's range test, the fast path alone (false:
   // the segment needs the rules) and the rules alone
+  static constexpr bool kFastAlwaysDone = true;  // fast_try / fast_two never decline a row that passed fast_ok
   static __device__ __forceinline__ bool fast_ok(const T (&P)[IN], const Params& w) { return box_fast_ok<T, D>(P, w); }
   static __device__ __forceinline__ bool fast_ok2(const T (&P)[IN], const Params& w) { return box_fast_ok2<T, D>(P, w); }
   static __device__ __forceinline__ bool fast_try(const T (&P)[IN], const Params& w, T (&Q)[OUT], bool& vis) {
@@ -131,6 +132,7 @@ struct IntOp {
 #pragma unroll
     for (int i = 0; i < NI; ++i) vis[i] = clip_one(P[i], w, Q[i]);
   }
+  static constexpr bool kFastAlwaysDone = true;
   static __device__ __forceinline__ bool fast_ok(const int32_t (&)[IN], const Params&) { return true; }
   static __device__ __forceinline__ bool fast_ok2(const int32_t (&)[IN], const Params&) { return true; }
   static __device__ __forceinline__ bool fast_two(const int32_t (&Pa)[IN], const int32_t (&Pb)[IN], const Params& w,
@@ -187,6 +189,7 @@ template <typename T, bool NDC> struct HomogOp : NoOutOfRange {  // NEXT-1: homo
   static __device__ __forceinline__ void clip_n(const T (&P)[NI][IN], const Params&, T (&Q)[NI][OUT], bool (&vis)[NI]) {
     homog_keptN<T, NDC, NI>(P, Q, vis);
   }
+  static constexpr bool kFastAlwaysDone = false;  // homog_fast may decline (a crossed endpoint's q_w <= 0)
   static __device__ __forceinline__ bool fast_ok(const T (&P)[IN], const Params&) { return homog_fast_ok<T>(P); }
   static __device__ __forceinline__ bool fast_ok2(const T (&P)[IN], const Params&) { return homog_fast_ok<T>(P); }
   static __device__ __forceinline__ bool fast_two(const T (&Pa)[IN], const T (&Pb)[IN], const Params&, T (&Qa)[OUT],
