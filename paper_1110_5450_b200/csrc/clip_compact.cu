@@ -1260,7 +1260,8 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
         fpar ^= 1u << b;
       }
     }
-    __syncwarp();  // the previous use of this region (a copy-out) is done
+    // (the previous use of this region, this warp's copy-out, is done: every lane has passed
+    // the scan's shuffles above after consuming its copy-out loads)
     int before = 0;
     int kbase[PW];  // list position of this lane's first kept segment of sub-tile j
 #pragma unroll
@@ -1397,7 +1398,10 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       }
 #endif
       vb = vb & actb;
-      __syncwarp();
+      // (the round's rows are all read before the ballots below, which every lane reaches only
+      // after consuming its loads, and ranks stay below the next round's positions: no
+      // __syncwarp needed between the reads and the stores)
+      if (CLIPSEG_PK_ILCOPY) __syncwarp();
       if (early) {
         copy_round();
         copy_round();
@@ -1447,7 +1451,7 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
         vis = Op::clip_one(row, w, res) & act;
       }
 #endif
-      __syncwarp();
+      if (CLIPSEG_PK_ILCOPY) __syncwarp();
       if (early) copy_round();
       const unsigned m = __ballot_sync(0xFFFFFFFFu, vis);
       if (vis) {
