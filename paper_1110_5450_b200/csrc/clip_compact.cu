@@ -1563,12 +1563,23 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
     // does once every count is in (CLIPSEG_PK_SCANPUB)
     int last = 0;
     if (!CLIPSEG_PK_SCANPUB && lane == 0) {
-      __threadfence_block();
-      last = atom_add_shared(&s_done[b], 1) == W - 1;
+#ifndef CLIPSEG_PK_DONEFENCE
+#define CLIPSEG_PK_DONEFENCE 2  // 0: fence.sc + relaxed add, 1: fence.acq_rel + add, 2: one acq_rel add (measured 5.422 -> 5.413 ms best)
+#endif
+      if constexpr (CLIPSEG_PK_DONEFENCE == 2) {
+        int old;
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(old) : "r"(smem_addr(&s_done[b])) : "memory");
+        last = old == W - 1;
+      } else {
+        if constexpr (CLIPSEG_PK_DONEFENCE == 1) asm volatile("fence.acq_rel.cta;" ::: "memory");
+        else __threadfence_block();
+        last = atom_add_shared(&s_done[b], 1) == W - 1;
+      }
     }
     if (!CLIPSEG_PK_SCANPUB) last = __shfl_sync(0xFFFFFFFFu, last, 0);
     if (last) {
-      __threadfence_block();
+      if constexpr (CLIPSEG_PK_DONEFENCE == 1) asm volatile("fence.acq_rel.cta;" ::: "memory");
+      else if constexpr (CLIPSEG_PK_DONEFENCE == 0) __threadfence_block();
       int c = (lane < W) ? ((volatile int*)s_cnt[b])[lane] : 0;
       if (W > 32 && lane + 32 < W) c += ((volatile int*)s_cnt[b])[lane + 32];
 #pragma unroll
