@@ -1576,7 +1576,21 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
         last = atom_add_shared(&s_done[b], 1) == W - 1;
       }
     }
-    if (!CLIPSEG_PK_SCANPUB) last = __shfl_sync(0xFFFFFFFFu, last, 0);
+#ifndef CLIPSEG_PK_LASTLANE
+#define CLIPSEG_PK_LASTLANE 1  // the last warp's lane 0 alone sums the counts and publishes (no warp broadcast)
+#endif
+    if (CLIPSEG_PK_LASTLANE && !CLIPSEG_PK_SCANPUB && CLIPSEG_PK_DONEFENCE == 2) {
+      if (last) {  // lane 0 only; the acq_rel add made the other warps' counts visible
+        int c = 0;
+#pragma unroll
+        for (int q = 0; q < W; ++q) c += ((volatile int*)s_cnt[b])[q];
+        st_relaxed(status + tile, kFlagA | (unsigned long long)c);
+        CLIP_TRACE(tile, 2, trace_now());
+      }
+      last = 0;
+    } else if (!CLIPSEG_PK_SCANPUB) {
+      last = __shfl_sync(0xFFFFFFFFu, last, 0);
+    }
     if (last) {
       if constexpr (CLIPSEG_PK_DONEFENCE == 1) asm volatile("fence.acq_rel.cta;" ::: "memory");
       else if constexpr (CLIPSEG_PK_DONEFENCE == 0) __threadfence_block();
@@ -1589,7 +1603,7 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
         CLIP_TRACE(tile, 2, trace_now());
       }
     }
-    __syncwarp();
+    if (!CLIPSEG_PK_LASTLANE) __syncwarp();
     if (lane == 0) mbar_arrive_a(mbc_a + 8 * b);
     // copy out iteration k - (NBUF-1), NBUF-1 tiles behind: its offsets are known by now
     b = cb;  // buffer of iteration k + 1 == buffer of iteration k - (NBUF-1)
