@@ -1386,10 +1386,23 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
         // round, pays that round: 0.148 -> 0.155 ms.  Voting first only after a batch that
         // broke out cost the headline 0.8 %: 5 more registers.)
         const bool ok = Op::fast_ok(ra, w) & Op::fast_ok(rb, w);
-        const bool done = Op::fast_two(ra, rb, w, qa, qb, va, vb);
-        if (!__all_sync(0xFFFFFFFFu, ok & done)) {
-          brk = true;
-          break;
+        if constexpr (S::K.vfirst) {  // (this instantiation votes before clipping)
+          if (!__all_sync(0xFFFFFFFFu, ok)) {
+            brk = true;
+            break;
+          }
+          if constexpr (Op::kFastAlwaysDone) {
+            Op::fast_two(ra, rb, w, qa, qb, va, vb);
+          } else if (!__all_sync(0xFFFFFFFFu, Op::fast_two(ra, rb, w, qa, qb, va, vb))) {
+            brk = true;
+            break;
+          }
+        } else {
+          const bool done = Op::fast_two(ra, rb, w, qa, qb, va, vb);
+          if (!__all_sync(0xFFFFFFFFu, ok & done)) {
+            brk = true;
+            break;
+          }
         }
       } else {
         Op::clip_two(ra, rb, w, qa, qb, va, vb);
@@ -1439,8 +1452,17 @@ __global__ void CLIPSEG_PK_BOUNDS(PackedShape<T, Op, INDEX>::kThreads) clip_comp
       bool vis;
       if constexpr (DEFER) {
         const bool ok = Op::fast_ok(row, w);
-        const bool done = Op::fast_try(row, w, res, vis);
-        if (!__all_sync(0xFFFFFFFFu, ok & done)) break;
+        if constexpr (S::K.vfirst) {
+          if (!__all_sync(0xFFFFFFFFu, ok)) break;
+          if constexpr (Op::kFastAlwaysDone) {
+            Op::fast_try(row, w, res, vis);
+          } else if (!__all_sync(0xFFFFFFFFu, Op::fast_try(row, w, res, vis))) {
+            break;
+          }
+        } else {
+          const bool done = Op::fast_try(row, w, res, vis);
+          if (!__all_sync(0xFFFFFFFFu, ok & done)) break;
+        }
         vis = vis & act;
       } else {
         vis = Op::clip_one(row, w, res) & act;

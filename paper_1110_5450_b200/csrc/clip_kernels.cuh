@@ -445,6 +445,8 @@ struct PackedKnobs {
   int warps, pw, nbuf, ilp;
   bool defer;    // exceptional rows end the fast rounds and are finished in deferred passes
   bool b0tiles;  // block 0 processes tiles too, its scan warp interleaving the global scanner
+  bool vfirst;   // deferred rounds vote on the range test before clipping (fp64: a wasted round costs
+                 // C3 fp64 0.52 -> 0.61 ms at 1e7; fp32 clips first, see clip_compact.cu)
 };
 // Block 0 taking tiles (its scan warp runs the global scanner and its own tile duties,
 // non-blocking): measured 3D 0.834 -> 0.829 ms at 1e8 and C3 fp32 0.149 -> 0.147 ms, but the
@@ -482,14 +484,14 @@ struct PackedKnobs {
 #endif
 template <typename T, class Op> __host__ __device__ constexpr PackedKnobs packed_knobs() {
   return Op::IN == 8      ? PackedKnobs{CLIPSEG_PKH_WARPS, CLIPSEG_PKH_PW, CLIPSEG_PKH_NBUF, CLIPSEG_PKH_ILP,
-                                     CLIPSEG_PKH_DEFER != 0, CLIPSEG_PK_B0TILES != 0}
+                                     CLIPSEG_PKH_DEFER != 0, CLIPSEG_PK_B0TILES != 0, false}
          : Op::IN == 6    ? PackedKnobs{CLIPSEG_PK3_WARPS, CLIPSEG_PK3_PW, CLIPSEG_PK3_NBUF, CLIPSEG_PK3_ILP,
-                                     CLIPSEG_PK3_DEFER != 0, CLIPSEG_PK3_B0TILES != 0}
+                                     CLIPSEG_PK3_DEFER != 0, CLIPSEG_PK3_B0TILES != 0, false}
          : sizeof(T) == 8 ? PackedKnobs{CLIPSEG_PKD_WARPS, CLIPSEG_PKD_PW, 3, CLIPSEG_PKD_ILP, CLIPSEG_PK_DEFER != 0,
-                                        CLIPSEG_PK_B0TILES != 0}
+                                        CLIPSEG_PK_B0TILES != 0, true}
                           : PackedKnobs{CLIPSEG_PK_WARPS, CLIPSEG_PK_PW, CLIPSEG_PK_NBUF, CLIPSEG_PK_ILP,
                                         CLIPSEG_PK_DEFER != 0 && !std::is_same<Op, IntOp>::value,
-                                        CLIPSEG_PK_B0TILES != 0};
+                                        CLIPSEG_PK_B0TILES != 0, false};
 }
 template <typename T, class Op> __host__ __device__ constexpr int compact_min_blocks() {
   return compact_headline<T, Op>() ? CLIPSEG_MINB_F32_2D : 1;
