@@ -471,13 +471,13 @@ struct PackedKnobs {
 #define CLIPSEG_PK_DEFER 1  // deferred passes for 2D fp32 / fp64 (measured: C3 fp32 1e7 0.237 -> 0.155 ms,
 #endif                      // fp64 0.580 -> 0.523, headline unchanged)
 #ifndef CLIPSEG_PK3_DEFER
-#define CLIPSEG_PK3_DEFER 0  // 3D fp32: C4 0.876 -> 0.882 ms with deferral
-#endif
+#define CLIPSEG_PK3_DEFER 1  // 3D fp32 (10 warps x 256): with deferral and two rows per lane C4 0.801 -> 0.794 ms
+#endif                       // (deferral alone 0.817, two rows alone 0.805)
 #ifndef CLIPSEG_PKH_DEFER
 #define CLIPSEG_PKH_DEFER 0  // homogeneous fp32: 1.17 -> 1.49 ms with deferral (spills)
 #endif
 #ifndef CLIPSEG_PK3_ILP
-#define CLIPSEG_PK3_ILP 1
+#define CLIPSEG_PK3_ILP 2
 #endif
 #ifndef CLIPSEG_PKD_ILP
 #define CLIPSEG_PKD_ILP 1
