@@ -389,7 +389,8 @@ template <typename T, class Op> __host__ __device__ constexpr bool compact_prefe
 // fp32 3D cuboid (C4): rows of 24 B; 10 compute warps with two sub-tiles (256 segments) per
 // batch (staging 10 warps x 3 x 6 KB, 156 registers for the 48-float prefetch) measured
 // 0.875 -> 0.832 ms at 1e8 against 15 warps x 128 segments (9 / 11 / 12 warps x 256: 0.93 /
-// 0.887 / 0.894; two rows per lane: 0.8325).
+// 0.887 / 0.894; two rows per lane: 0.8325; after the synchronisation clean-up 9 / 11 / 12
+// warps x 256: 0.873 / 0.879 / 0.958 vs 0.775).
 #ifndef CLIPSEG_PACKED_F32_3D
 #define CLIPSEG_PACKED_F32_3D 1
 #endif
@@ -449,14 +450,15 @@ struct PackedKnobs {
                  // C3 fp64 0.52 -> 0.61 ms at 1e7; fp32 clips first, see clip_compact.cu)
 };
 // Block 0 taking tiles (its scan warp runs the global scanner and its own tile duties,
-// non-blocking): measured 3D 0.834 -> 0.829 ms at 1e8 and C3 fp32 0.149 -> 0.147 ms, but the
-// headline 5.586 -> 5.624 ms best at 1e9 — the scanner, on whose latency every copy-out
-// waits, then shares its SM with 15 compute warps.  On for 3D only.
+// non-blocking): measured the headline 5.586 -> 5.624 ms best at 1e9 — the scanner, on whose
+// latency every copy-out waits, then shares its SM with the compute warps — and, once the
+// hot loop lost its needless warp synchronisation, 3D 0.775 -> 0.798 ms at 1e8 (before:
+// 0.834 -> 0.829).  Off.
 #ifndef CLIPSEG_PK_B0TILES
 #define CLIPSEG_PK_B0TILES 0
 #endif
 #ifndef CLIPSEG_PK3_B0TILES
-#define CLIPSEG_PK3_B0TILES 1
+#define CLIPSEG_PK3_B0TILES 0
 #endif
 #ifndef CLIPSEG_PK_COPYW
 #define CLIPSEG_PK_COPYW 0  // copy warps in the service warpgroup (0: compute warps copy their own batches)
