@@ -72,6 +72,19 @@ def main():
     ntl = np.array([(blk == bb).sum() for bb in np.unique(blk)])
     res["block_busy_us"] = {p: round(float(np.percentile(busy, p)), 2) for p in (10, 50, 90)}
     res["block_tiles"] = {p: int(np.percentile(ntl, p)) for p in (10, 50, 90)}
+    # copy-out waits: a block copies tile t_i out right after publishing t_{i+2}'s aggregate;
+    # the wait is max(0, copy start of t_i - A of t_{i+2}) (warp 0's view)
+    tiles_ok = np.nonzero(ok)[0]
+    waits, spans = [], []
+    for bb in np.unique(blk):
+        tl = tiles_ok[blk == bb]
+        tl = tl[np.argsort(t[tl, 0])]  # claim order
+        for i in range(len(tl) - 2):
+            waits.append(max(0, int(t[tl[i], 6]) - int(t[tl[i + 2], 2])))
+        spans.append(float(t[tl, 6].max() - t[tl, 1].min()))
+    waits = np.array(waits, dtype=np.float64) / 1000
+    res["copy_wait_us"] = {p: round(float(np.percentile(waits, p)), 3) for p in (50, 75, 90, 99)}
+    res["copy_wait_share_of_block_span"] = round(float(waits.sum() / (np.sum(spans) / 1000)), 4)
     res["first_start_us"] = float(tr[:, 1].min()) / 1000
     res["last_A_us"] = float(tr[:, 2].max()) / 1000
     # lateness of predecessor: A time of t-1 minus A time of t
