@@ -149,5 +149,25 @@ __device__ __forceinline__ uint32_t clip_int_one(int32_t x0, int32_t y0, int32_t
   return clip_int_core<int64_t>(X0, Y0, X1, Y1, win, q);
 }
 
+// Two kept (in-range) segments per lane, the packed compacting kernel's rounds: the 32-bit
+// path runs on both rows first (branch-free; its values are unused for a row outside its
+// range), then one warp vote sends the rare warps holding a wide row to the 64-bit path
+// for those rows only.
+__device__ __forceinline__ bool int_small(int32_t x0, int32_t y0, int32_t x1, int32_t y1, bool small_win) {
+  const uint32_t m = max(max((uint32_t)x0 + (uint32_t)kSmall, (uint32_t)y0 + (uint32_t)kSmall),
+                         max((uint32_t)x1 + (uint32_t)kSmall, (uint32_t)y1 + (uint32_t)kSmall));
+  return small_win && m <= 2u * kSmall;
+}
+__device__ __forceinline__ void clip_int_two(const int32_t (&a)[4], const int32_t (&b)[4], int4 win, bool small_win,
+                                             int32_t (&qa)[4], int32_t (&qb)[4], bool& va, bool& vb) {
+  const bool sa = int_small(a[0], a[1], a[2], a[3], small_win), sb = int_small(b[0], b[1], b[2], b[3], small_win);
+  va = clip_int_small(a[0], a[1], a[2], a[3], win, qa) == 1u;
+  vb = clip_int_small(b[0], b[1], b[2], b[3], win, qb) == 1u;
+  if (!__all_sync(0xFFFFFFFFu, sa & sb)) {
+    if (!sa) va = clip_int_core<int64_t>(a[0], a[1], a[2], a[3], win, qa) == 1u;
+    if (!sb) vb = clip_int_core<int64_t>(b[0], b[1], b[2], b[3], win, qb) == 1u;
+  }
+}
+
 }  // namespace intclip
 }  // namespace clipseg

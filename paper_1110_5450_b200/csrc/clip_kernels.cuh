@@ -123,8 +123,15 @@ struct IntOp {
   }
   static __device__ __forceinline__ void clip_two(const int32_t (&Pa)[IN], const int32_t (&Pb)[IN], const Params& w,
                                                   int32_t (&Qa)[OUT], int32_t (&Qb)[OUT], bool& va, bool& vb) {
-    va = clip_one(Pa, w, Qa);
-    vb = clip_one(Pb, w, Qb);
+#ifndef CLIPSEG_INT_TWO
+#define CLIPSEG_INT_TWO 1  // 32-bit path on both rows, then a vote (0: two per-lane branching clips)
+#endif
+    if constexpr (CLIPSEG_INT_TWO) {
+      intclip::clip_int_two(Pa, Pb, w.win, w.small != 0, Qa, Qb, va, vb);
+    } else {
+      va = clip_one(Pa, w, Qa);
+      vb = clip_one(Pb, w, Qb);
+    }
   }
   template <int NI>
   static __device__ __forceinline__ void clip_n(const int32_t (&P)[NI][IN], const Params& w, int32_t (&Q)[NI][OUT],

@@ -1,2 +1,2 @@
-for mode in 0 1; do for B in 4 32; do for x0 in 0 4 12 1 2 3 37; do timeout 30 ./build/tma_probe2 $B $x0 $mode; done; done; done > gpurun_out/tma_probe2_cases.txt 2>&1
-cat gpurun_out/tma_probe2_cases.txt
+CLIPSEG_LIB=build/libclipseg_it2.so timeout 600 python -m pytest tests/test_gpu_int.py -m gpu -q -x > gpurun_out/r02af_tests.txt 2>&1; tail -1 gpurun_out/r02af_tests.txt
+PROBE=scripts/int_probe.py bash scripts/ab_args.sh 3 "--reps 20" it0 it2
