@@ -1,2 +1,3 @@
-CLIPSEG_LIB=build/libclipseg_ns16.so timeout 600 python -m pytest tests/test_gpu_parity.py tests/test_gpu_canary.py tests/test_gpu_defer.py -m gpu -q -x > gpurun_out/r02ah_tests.txt 2>&1; tail -1 gpurun_out/r02ah_tests.txt
-timeout 900 bash scripts/ab_long.sh 2 cur ns16 ns15
+# scratch A/B command list run through gpurun during round 2 (the last one is kept); see
+# profiles/r02_summary.md for the measurements
+timeout 1200 bash scripts/ab_long.sh 2 cur sp1 sp4 bo64
