@@ -1,3 +1,3 @@
-# scratch A/B command list run through gpurun during round 2 (the last one is kept); see
-# profiles/r02_summary.md for the measurements
-timeout 1200 bash scripts/ab_long.sh 2 cur sp1 sp4 bo64
+# final sanity of the committed tree: GPU tests + smoke
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/r02_final_tests.txt 2>&1; tail -1 gpurun_out/r02_final_tests.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
